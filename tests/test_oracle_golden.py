@@ -1,0 +1,129 @@
+"""Pin the CPU oracle against golden vectors produced by the reference itself.
+
+The fixtures (tests/golden/*.npz) were written by tests/golden/make_golden.py, which
+runs vegsplat's public API; the oracle must reproduce every integer output
+bit-exactly and the float outputs to within fp64 re-association noise (float64
+blends) or the fp32 storage ulp (float32 blends)."""
+
+import numpy as np
+import pytest
+
+import goldens as G
+from oracle import vegs_oracle as O
+from paper_2504_13339_b200.constants import DEFAULT_SETTINGS as S
+
+FWD = [("c0_f32", np.float32, False), ("c0_f64", np.float64, False),
+       ("c0_aux_f32", np.float32, True), ("dense_f32", np.float32, False)]
+
+
+@pytest.fixture(scope="module", params=FWD, ids=[f[0] for f in FWD])
+def fwd_case(request):
+    name, dt, aux = request.param
+    d = G.load(name)
+    img, st = O.render_with_state(G.gs_of(d), G.tf_of(d), G.cam_of(d["cam"]), tuple(d["bg"]), S, aux, dt)
+    return name, dt, aux, d, img, st
+
+
+def test_integer_outputs_bit_exact(fwd_case):
+    name, dt, aux, d, img, st = fwd_case
+    assert np.array_equal(st["kept"], d["kept"])
+    assert np.array_equal(st["proj"]["rect"], d["rect"])
+    assert np.array_equal(st["order"], d["order"])
+    assert np.array_equal(st["tile_start"], d["tile_start"])
+    assert np.array_equal(st["tile_end"], d["tile_end"])
+    assert np.array_equal(st["out_last"], d["out_last"])
+    assert np.array_equal(st["n_contrib"], d["n_contrib"])
+
+
+def test_float_outputs(fwd_case):
+    name, dt, aux, d, img, st = fwd_case
+    tol = 1e-6 if dt == np.float32 else 1e-13
+    assert np.abs(st["proj"]["depth"] - d["depth"]).max() <= 1e-14
+    assert np.array_equal(st["inst_pmin"], d["inst_pmin"]) or np.abs(st["inst_pmin"] - d["inst_pmin"]).max() < tol
+    assert np.abs(st["out_t"] - d["out_t"]).max() <= tol
+    assert np.abs(img["rgb"] - d["rgb"]).max() <= tol
+    if aux:
+        for k in ("depth", "normal", "attrs"):
+            assert np.abs(img[k] - d[k + "_plane"]).max() <= 10 * tol
+
+
+def test_backward_gradients(fwd_case):
+    name, dt, aux, d, img, st = fwd_case
+    kw = {k: d["probe_" + k] for k in ("rgb", "alpha", "depth", "normal", "attrs") if "probe_" + k in d}
+    g = O.rasterize_backward(st, **kw)
+    tol = 1e-6 if dt == np.float32 else 1e-12
+    for k in O.GRAD_CLASSES:
+        assert G.norm_rel(g[k], d["grad_" + k]) <= tol, k
+    assert np.array_equal(g["visible"], d["grad_visible"])
+    assert G.norm_rel(g["viewspace_norm"], d["grad_viewspace_norm"]) <= tol
+
+
+def test_termination_and_clamp_are_exercised():
+    d = G.load("dense_f32")
+    # some pixels terminate (T pinned just above the 1e-4 stop) and have many contributors
+    assert d["out_t"].min() < 2e-4 and d["n_contrib"].max() > 50
+
+
+@pytest.mark.parametrize("seed", range(8))
+def test_reference_gradcheck_scenes(seed):
+    d = G.load("gradcheck_scenes")
+    p = f"s{seed}_"
+    gs = G.gs_of(d, p + "gs_")
+    img, st = O.render_with_state(gs, G.tf_of(d, p + "tf_"), G.cam_of(d[p + "cam"]), tuple(d[p + "bg"]),
+                                  S, True, np.float64)
+    assert np.abs(img["rgb"] - d[p + "rgb"]).max() < 1e-12
+    assert np.abs(img["depth"] - d[p + "depth_plane"]).max() < 1e-12
+    g = O.rasterize_backward(st, **{k: d[p + "probe_" + k] for k in ("rgb", "alpha", "depth", "normal", "attrs")})
+    for k in O.GRAD_CLASSES:
+        assert G.norm_rel(g[k], d[p + "grad_" + k]) <= 1e-11, k
+
+
+@pytest.mark.parametrize("seed", range(5))
+def test_raw_blend_boundary(seed):
+    d = G.load("blend_scenes")
+    p = f"s{seed}_"
+    data = {k: d[p + k] for k in ("mean2d", "conic", "alpha_base", "depth", "rect", "channels")}
+    w, h = (int(x) for x in d[p + "wh"])
+    img, st = O.rasterize_forward(data, w, h, d[p + "bg"], S, np.float64)
+    assert np.array_equal(st["order"], d[p + "order"])
+    assert np.array_equal(st["out_last"], d[p + "out_last"])
+    assert np.abs(img["rgb"] - d[p + "rgb"]).max() < 1e-13
+
+
+def test_tf_lookup_bitwise():
+    d = G.load("tf_lookup")
+    for j in range(5):
+        ts, q = d[f"k{j}_ts"], d[f"k{j}_q"]
+        assert np.array_equal(O.tf_lookup(ts, d[f"k{j}_op"], q), d[f"k{j}_eval_op"])
+        assert np.array_equal(O.tf_lookup(ts, d[f"k{j}_col"], q), d[f"k{j}_eval_col"])
+        assert np.array_equal(O.tf_slope(ts, d[f"k{j}_op"], q), d[f"k{j}_d_op"])
+        assert np.array_equal(O.tf_slope(ts, d[f"k{j}_col"], q), d[f"k{j}_d_col"])
+
+
+@pytest.mark.parametrize("dt", ["f32", "f64"])
+def test_loss(dt):
+    d = G.load("loss")
+    total, grad, l1, mssim = O.l1_ssim_loss(d[f"{dt}_x"], d[f"{dt}_y"], 0.2)
+    tol = 1e-6 if dt == "f32" else 1e-12
+    assert abs(total - float(d[f"{dt}_total"])) <= tol
+    assert abs(mssim - float(d[f"{dt}_ssim"])) <= tol
+    assert G.norm_rel(grad, d[f"{dt}_grad"]) <= 10 * tol
+
+
+def _cfg():
+    return dict(iterations=100, lr_position=1.6e-4, lr_position_final=1.6e-6, lr_scale=5e-3,
+                lr_rotation=1e-3, lr_value=0.00025, lr_weight=0.025, lr_lighting=5e-3)
+
+
+def test_adam_three_steps():
+    d = G.load("adam")
+    params = {k: d["in_" + k].astype(np.float64).copy() for k in O.GRAD_CLASSES}
+    m = {k: np.zeros_like(v) for k, v in params.items()}
+    v = {k: np.zeros_like(p) for k, p in params.items()}
+    for it in (1, 2, 3):
+        lrs = O.learning_rates(_cfg(), it)
+        for k in O.GRAD_CLASSES:
+            O.adam_update(params[k], d[f"g{it}_{k}"], m[k], v[k], it, lrs[k])
+    for k in O.GRAD_CLASSES:
+        assert np.array_equal(params[k], d["out_" + k]), k
+        assert np.array_equal(m[k], d["m_" + k]) and np.array_equal(v[k], d["v_" + k])
