@@ -1,0 +1,407 @@
+#!/usr/bin/env python
+"""Benchmark: BASELINE.json config 2 -- the 1M-Gaussian, 16-view x 1024^2 training step.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+
+One step = every view of the step rendered (preprocess -> bin/sort -> composite),
+scored (0.8 L1 + 0.2 (1-SSIM), the reference's convention), back-propagated (composite
+backward -> per-Gaussian float64 gradients), the flat gradient buffer all-reduced across
+ranks (NCCL, N > 1) and Adam applied.  The 16 views are sharded across the N ranks
+(strong scaling: total work is fixed).  Inputs are synthetic (scenes.py, seeded);
+targets are renders of the seed-1 64-blob ground-truth set.  The working set (152 MB
+of float64 parameters, ~24M tile instances per view) is far larger than L2, so no flush
+is needed between steps.
+
+Reported on rank 0 as one JSON line: ``value`` = steps/s (device-timed, max over ranks),
+``e2e`` = the same step through the public API with the step's target images copied
+from pinned host memory each step and the loss read back, ``render_mpx_s`` = forward
+render throughput over the same views, ``roofline`` for the dominant kernel (CUDA events
+on its launching stream inside the timed region), ``cpu_baseline`` = the CPU oracle on a
+bounded sample of the same workload, ``clocks`` sampled with nvidia-smi during the
+timed region.
+
+``--impl reference`` times the reference algorithm's CPU implementation instead: the
+reference is pure numpy + numba (no GPU code), restated in oracle/
+(numpy + OpenMP C kernels, pinned to the reference's golden vectors); it runs on all
+host cores, one bounded sample (one of the 16 views of a step, extrapolated) per step.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "train steps/s at 1M Gaussians (config 2: 16 views/step @1024x1024)"
+UNIT = "steps/s"
+WORKLOAD = "c2"
+VIEWS_PER_STEP = 16
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=("b200", "reference"), default="b200")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--render-frames", type=int, default=5)
+    ap.add_argument("--cpu-budget-s", type=float, default=60.0)
+    return ap.parse_args()
+
+
+def config_block(world: int) -> dict:
+    return {"workload": "c2: 1M Gaussians (seed 0) fit to renders of a 1M-Gaussian 64-blob set (seed 1); "
+                        "16 views/step at 1024x1024, 256-knot TF; step = render + L1/SSIM + backward "
+                        "+ all-reduce + Adam",
+            "n_gaussians": 1_000_000, "views_per_step": VIEWS_PER_STEP, "width": 1024, "height": 1024,
+            "loss": "0.8*L1 + 0.2*(1-SSIM) (reference (1-lambda) weighting)",
+            "parallelism": f"view-sharded dp{world}", "l2": "inputs larger than L2 (no flush needed)"}
+
+
+def peaks() -> tuple[float, str]:
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        try:
+            return float(json.loads(p.read_text())["hbm_gbs"]), "measured"
+        except Exception:
+            pass
+    return 6650.0, "fallback"
+
+
+# -- clocks sampled during the timed region ---------------------------------------------
+
+class ClockSampler:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.proc = None
+        self.path = None
+
+    def start(self):
+        fd, self.path = tempfile.mkstemp(suffix=".csv")
+        os.close(fd)
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except OSError:
+            self.proc = None
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        self.proc.wait(timeout=10)
+        rows = [r.split(", ") for r in Path(self.path).read_text().splitlines() if r.strip()]
+        os.unlink(self.path)
+        sm = [float(r[1]) for r in rows if len(r) >= 9 and r[1].replace(".", "").isdigit()]
+        smax = [float(r[2]) for r in rows if len(r) >= 9 and r[2].replace(".", "").isdigit()]
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        reasons = sorted({names[i] for r in rows if len(r) >= 9 for i in range(4) if r[5 + i].strip() == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(smax) if smax else None,
+                "reasons": reasons, "samples": len(rows)}
+
+
+# -- per-launch CUDA-event timing of the compositing kernels -----------------------------
+
+class KernelTimer:
+    """Events recorded on the current stream around each C-ABI launch group."""
+
+    def __init__(self, rz, names=("vegs_composite_forward", "vegs_composite_backward")):
+        import torch
+
+        self.torch = torch
+        self.rz = rz
+        self.names = set(names)
+        self.open: dict = {}
+        self.done: dict = {n: [] for n in names}
+
+    def mark(self, name, begin):
+        if name not in self.names:
+            return
+        ev = self.torch.cuda.Event(enable_timing=True)
+        ev.record()
+        if begin:
+            self.open[name] = (ev, self.rz.last_counts)
+        else:
+            start, counts = self.open.pop(name)
+            self.done[name].append((start, ev, counts))
+
+    def summary(self) -> dict:
+        out = {}
+        for name, recs in self.done.items():
+            if recs:
+                ms = [a.elapsed_time(b) for a, b, _ in recs]
+                out[name] = dict(launches=len(recs), avg_ms=sum(ms) / len(ms), total_ms=sum(ms),
+                                 counts=[c for _, _, c in recs])
+        return out
+
+
+def algorithmic_bytes(name: str, n_kept: int, n_inst: int, pixels: int, n_ch: int = 3) -> float:
+    """SURVEY.md §8(d) minimum HBM bytes per composite launch."""
+    per_inst = 4 + 28 + 4 * n_ch
+    per_px = 4 * n_ch + 4 + 4
+    b = n_inst * per_inst + pixels * per_px
+    if name == "vegs_composite_backward":
+        b += n_kept * (6 + n_ch) * 4 * 2
+    return float(b)
+
+
+# -- the B200 arm -------------------------------------------------------------------------
+
+def run_b200(args) -> None:
+    import torch
+    import torch.distributed as dist
+
+    from paper_2504_13339_b200 import scenes
+    from paper_2504_13339_b200.device import DeviceTF, Rasterizer
+    from paper_2504_13339_b200.parallel import init_from_env, shard_views
+    from paper_2504_13339_b200.train import TrainConfig, Trainer, View
+
+    rank, world, local = init_from_env("nccl")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    learned, truth, tf, cams = scenes.config_scene(WORKLOAD)
+    mine = shard_views(VIEWS_PER_STEP, rank, world)
+    dtf = DeviceTF(tf, dev)
+
+    # ground-truth targets for this rank's views (setup, untimed)
+    rz_gt = Rasterizer(pooled=True)
+    gt_params = torch.from_numpy(truth.pack()).to(dev)
+    targets = []
+    for i in mine:
+        fr = rz_gt.forward(gt_params, len(truth), dtf, cams[i])
+        targets.append(fr.out_img.view(cams[i].height, cams[i].width, 3).clone())
+    del rz_gt, gt_params
+    host_targets = [t.cpu().pin_memory() for t in targets]
+    torch.cuda.synchronize()
+
+    group = dist.group.WORLD if world > 1 else None
+    trainer = Trainer(learned, TrainConfig(iterations=30000), group=group)
+    views = [View(cams[i], dtf, targets[j]) for j, i in enumerate(mine)]
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    def max_over_ranks(x: float) -> float:
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    for _ in range(max(args.warmup, 3)):
+        trainer.step(views, total_views=VIEWS_PER_STEP)
+    torch.cuda.synchronize()
+
+    # ---- timed region: device-resident training steps
+    timer = KernelTimer(trainer.rz)
+    trainer.rz.timer = timer
+    launches0 = trainer.rz.launches
+    clocks = ClockSampler(local)
+    barrier()
+    torch.cuda.synchronize()
+    clocks.start()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    loss = None
+    for _ in range(args.steps):
+        loss = trainer.step(views, total_views=VIEWS_PER_STEP)
+    e1.record()
+    torch.cuda.synchronize()
+    barrier()
+    clk = clocks.stop()
+    trainer.rz.timer = None
+    ms = max_over_ranks(e0.elapsed_time(e1))
+    launches = trainer.rz.launches - launches0 + args.steps * (2 * len(views) + 1)  # + loss, Adam
+    ms_step = ms / args.steps
+    value = 1000.0 / ms_step
+    ksum = timer.summary()
+    loss_val = float(loss.item())
+    trainer.check_finite()
+
+    # ---- forward render throughput over the same views
+    rz = trainer.rz
+    for _ in range(2):
+        for v in views:
+            rz.forward(trainer.params, trainer.n, dtf, v.camera)
+    barrier()
+    torch.cuda.synchronize()
+    r0, r1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    r0.record()
+    for _ in range(args.render_frames):
+        for v in views:
+            rz.forward(trainer.params, trainer.n, dtf, v.camera)
+    r1.record()
+    torch.cuda.synchronize()
+    barrier()
+    rms = max_over_ranks(r0.elapsed_time(r1))
+    px = args.render_frames * VIEWS_PER_STEP * 1024 * 1024
+    render_mpx_s = px / (rms / 1000.0) / 1e6
+
+    # ---- end to end through the public API with host buffers
+    h2d = sum(t.numel() * t.element_size() for t in host_targets)
+    barrier()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s0.record()
+    for _ in range(args.steps):
+        for t_dev, t_host in zip(targets, host_targets):
+            t_dev.copy_(t_host, non_blocking=True)
+        lv = trainer.step(views, total_views=VIEWS_PER_STEP).item()  # D2H of the loss
+    s1.record()
+    torch.cuda.synchronize()
+    wall = time.perf_counter() - t0
+    barrier()
+    e2e_ms = max_over_ranks(max(s0.elapsed_time(s1), wall * 1000.0)) / args.steps
+    e2e = {"value": 1000.0 / e2e_ms, "unit": UNIT, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": 8,
+           "ms_per_step": e2e_ms}
+
+    if rank != 0:
+        dist.destroy_process_group() if world > 1 else None
+        return
+
+    # ---- roofline of the dominant kernel (largest share of the step)
+    peak, peak_kind = peaks()
+    dom = max(ksum, key=lambda k: ksum[k]["total_ms"]) if ksum else None
+    roof = None
+    if dom:
+        rec = ksum[dom]
+        byts = [algorithmic_bytes(dom, nk, ni, 1024 * 1024) for nk, ni in rec["counts"]]
+        avg_bytes = sum(byts) / len(byts)
+        achieved = avg_bytes / (rec["avg_ms"] / 1000.0) / 1e9
+        traffic = None
+        prof = ROOT / "profiles" / "ncu_dram_bytes.json"
+        if prof.exists():
+            traffic = json.loads(prof.read_text()).get(dom)
+        roof = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "peak_source": peak_kind,
+                "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
+                "algorithmic_bytes_per_launch": avg_bytes, "avg_launch_ms": rec["avg_ms"],
+                "share_of_step": rec["total_ms"] / ms / 1.0,
+                "note": "compositing is CUDA-core (FP32/FP64 + MUFU) bound, not HBM bound (SURVEY §8(d))"}
+    kernels = {k: {"avg_ms": v["avg_ms"], "launches": v["launches"], "share_of_step": v["total_ms"] / ms,
+                   "avg_instances": sum(c[1] for c in v["counts"]) / len(v["counts"])}
+               for k, v in ksum.items()}
+
+    cpu = None
+    if world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline_sample(learned, tf, cams[mine[0]], targets[0].cpu().numpy(), args.cpu_budget_s)
+
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": max(args.warmup, 3), "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f32+f64", "data": "synthetic (seeded, scenes.py)",
+            "config": config_block(world), "e2e": e2e, "render_mpx_s": render_mpx_s, "loss": loss_val,
+            "gpu_launches": int(launches), "roofline": roof, "kernels": kernels, "cpu_baseline": cpu,
+            "clocks": clk}
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+# -- the CPU arm (oracle restatement of the reference algorithm) -------------------------
+
+def _oracle_view(O, S, learned, tf, cam, target):
+    t0 = time.perf_counter()
+    img, st = O.render_with_state(learned, tf, cam, (1.0, 1.0, 1.0), S, False, np.float32)
+    total, grad, _, _ = O.l1_ssim_loss(img["rgb"], target, 0.2)
+    O.rasterize_backward(st, grad)
+    return time.perf_counter() - t0
+
+
+def _oracle_adam(O, n):
+    rng = np.random.default_rng(0)
+    p = rng.normal(size=19 * n)
+    g = rng.normal(size=19 * n)
+    m = np.zeros_like(p)
+    v = np.zeros_like(p)
+    t0 = time.perf_counter()
+    O.adam_update(p, g, m, v, 1, 1e-3)
+    return time.perf_counter() - t0
+
+
+def cpu_baseline_sample(learned, tf, cam, target, budget_s: float, max_views: int = 3) -> dict:
+    os.environ.setdefault("OMP_NUM_THREADS", str(os.cpu_count() or 1))
+    from oracle import vegs_oracle as O
+    from paper_2504_13339_b200.constants import DEFAULT_SETTINGS as S
+
+    O.lib()
+    times = []
+    t_start = time.perf_counter()
+    while len(times) < max_views and (not times or time.perf_counter() - t_start + times[-1] < budget_s):
+        times.append(_oracle_view(O, S, learned, tf, cam, target))
+    t_view = statistics.median(times)
+    t_adam = _oracle_adam(O, len(learned))
+    step_s = VIEWS_PER_STEP * t_view + t_adam
+    return {"value": 1.0 / step_s, "unit": UNIT, "cores": int(os.environ.get("OMP_NUM_THREADS", "1")),
+            "kind": "port", "sample": f"{len(times)} x one of the {VIEWS_PER_STEP} views of a c2 step "
+                                      f"(render+loss+backward, median {t_view:.2f} s) x{VIEWS_PER_STEP} "
+                                      f"+ 1M-Gaussian Adam ({t_adam:.2f} s)",
+            "s_per_step": step_s}
+
+
+def run_reference(args) -> None:
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return  # the reference is single-process; other ranks exit without work
+    os.environ.setdefault("OMP_NUM_THREADS", str(os.cpu_count() or 1))
+    from oracle import vegs_oracle as O
+    from paper_2504_13339_b200 import scenes
+    from paper_2504_13339_b200.constants import DEFAULT_SETTINGS as S
+
+    O.lib()
+    learned, truth, tf, cams = scenes.config_scene(WORKLOAD)
+    cam = cams[0]
+    # target of view 0: the ground-truth set rendered by the same CPU implementation
+    img_t, _ = O.render_with_state(truth, tf, cam, (1.0, 1.0, 1.0), S, False, np.float32)
+    target = img_t["rgb"]
+    t_adam = _oracle_adam(O, len(learned))
+    times = []
+    budget = args.cpu_budget_s * 3
+    t0 = time.perf_counter()
+    for _ in range(max(args.steps, 1)):
+        times.append(_oracle_view(O, S, learned, tf, cam, target))
+        if time.perf_counter() - t0 > budget:
+            break
+    t_view = statistics.median(times)
+    step_s = VIEWS_PER_STEP * t_view + t_adam
+    value = 1.0 / step_s
+    cores = int(os.environ["OMP_NUM_THREADS"])
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": len(times), "warmup": 0, "ms_per_step": step_s * 1000.0, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64 (f32 planes)", "data": "synthetic (seeded)",
+            "config": config_block(1),
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
+                             "sample": f"{len(times)} timed samples; each = one of the {VIEWS_PER_STEP} views of a "
+                                       f"c2 step (render+loss+backward, median {t_view:.2f} s) x{VIEWS_PER_STEP} + "
+                                       f"1M-Gaussian Adam ({t_adam:.2f} s)"},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_b200(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,205 @@
+/*
+ * vegsplat_b200 -- C-ABI of the B200-native differentiable VEG rasteriser.
+ *
+ * Every entry point takes plain device pointers, sizes and a cudaStream_t passed as
+ * void*, never throws, and returns an int status (VEGS_OK or a negative error).  All
+ * memory is owned by the caller (the Python host allocates it as torch tensors);
+ * functions needing scratch follow the CUB convention: call once with ws == NULL to
+ * receive the byte count in *ws_bytes.
+ *
+ * Reference interfaces replaced (paths under /root/reference/pkg/src/vegsplat/):
+ *   vegs_blend_forward          raster/kernels.py:26-100  blend_forward(...)      (same arguments)
+ *   vegs_blend_backward         raster/kernels.py:103-208 blend_backward(...)     (same arguments)
+ *   vegs_preprocess_forward     raster/shading.py:52-82 shade + raster/projection.py:69-176 project
+ *                               + raster/pipeline.py:137-160 build_splat_data, pipeline.py:207-215 (pmin,
+ *                               f32 instance cast)
+ *   vegs_bin_count / vegs_bin_sort
+ *                               raster/pipeline.py:163-194 _build_instances (repeat + lexsort + searchsorted)
+ *   vegs_composite_forward      raster/pipeline.py:197-237 rasterize_forward (tile blend on the splat table)
+ *   vegs_composite_backward     raster/pipeline.py:291-305 (blend_backward on the splat table, per-instance
+ *                               rows written in duplicate order for the deterministic reduction)
+ *   vegs_preprocess_backward    raster/pipeline.py:307-366 (np.add.at reduction, project_backward
+ *                               projection.py:186-277, shade_backward shading.py:97-176, GradientSet)
+ *   vegs_loss_l1_ssim           loss.py:80-168 ssim / ssim_backward / compute_loss (regularisers off)
+ *   vegs_adam_step              train.py:176-195 adam_step (+ learning_rates :156-173 on the host)
+ *   vegs_tf_eval                transfer.py:91-127 eval_opacity / eval_color / d_*_dv
+ */
+#ifndef VEGSPLAT_B200_H
+#define VEGSPLAT_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define VEGS_OK 0
+#define VEGS_ERR_ARG (-1)      /* bad argument (null pointer, unsupported size/tile/channels) */
+#define VEGS_ERR_CUDA (-2)     /* a CUDA launch or runtime call failed */
+#define VEGS_ERR_CAPACITY (-3) /* caller buffer too small */
+
+#define VEGS_MAX_KNOTS 1024
+
+/* Per-view camera constants, computed on the host exactly as camera.py:54-90 does. */
+typedef struct {
+    double position[3];
+    double rot[9];   /* world->camera rows: right, up, forward (positive depth in front) */
+    double focal;    /* 0.5 * height / tan(fov_y / 2) */
+    double tan_x;    /* tan(fov_y / 2) * width / height */
+    double tan_y;    /* tan(fov_y / 2) */
+    double near_z;
+    int32_t width;
+    int32_t height;
+} VegsCamera;
+
+/* raster/constants.py:15-25 */
+typedef struct {
+    double dilation;
+    double alpha_clamp;
+    double alpha_skip;
+    double transmittance_stop;
+    double radius_sigma;
+    double rect_margin_px;
+    double cull_alpha;
+    double frustum_limit;
+    int32_t tile_size; /* must be 16: one 256-thread CTA per tile */
+    int32_t pad_;
+} VegsSettings;
+
+/* Transfer-function knot blob (transfer.py:30-88), float64:
+ * [ts_op(n_op) | op(n_op) | ts_col(n_col) | r(n_col) | g(n_col) | b(n_col)] */
+typedef struct {
+    const double *blob;
+    int32_t n_opacity;
+    int32_t n_color;
+} VegsTF;
+
+/* Per-Gaussian splat table written by vegs_preprocess_forward (n entries, indexed by
+ * Gaussian id; entries of culled Gaussians are left untouched except tiles = 0).
+ * record: n x rec_stride values of the blend storage type (float or double):
+ *   [mx, my, conic_a, conic_b, conic_c, alpha_base, pmin, ch_0 .. ch_{C-1}, pad]
+ * rec_stride = round_up(7 + C, 4). */
+typedef struct {
+    void *record;            /* float or double, see store_f64 */
+    int32_t *rect;           /* n x 4: x0, x1, y0, y1 (exclusive ends) */
+    uint32_t *tiles;         /* n: tiles touched (0 = not kept) */
+    uint64_t *depth_key;     /* n: order-preserving key of the float64 depth (UINT64 max when not kept) */
+    /* optional float64 views for the reference-shaped API (NULL to skip) */
+    double *mean2d;          /* n x 2 */
+    double *conic;           /* n x 3 */
+    double *depth;           /* n */
+    double *alpha_base;      /* n (written for every Gaussian, kept or not) */
+    double *color;           /* n x 3 shaded colour (every Gaussian) */
+    double *radius;          /* n */
+    uint8_t *visible;        /* n: alpha_base >= cull (shading.py:75) */
+    double *aux;             /* n x 24 shading / projection caches (ShadeResult, ProjectResult):
+                                v, w, opacity, cmap[3], light[3], light_dist, n_hat[3], n_norm, ndotl,
+                                ka, kd, ks, beta, spec_pow, cov2d[3] (a, b, c incl. dilation), pad */
+} VegsSplatTable;
+
+/* ---- TF lookup (tests / host API) ------------------------------------------------- */
+int vegs_tf_eval(const double *ts, const double *vals, int32_t n_knots, int32_t n_cols,
+                 const double *query, int64_t n_query, int32_t derivative, double *out,
+                 void *stream);
+
+/* ---- preprocess ------------------------------------------------------------------- */
+int vegs_preprocess_forward(const double *params, int64_t n, const VegsCamera *cam,
+                            const VegsTF *tf, const VegsSettings *st, int32_t n_channels,
+                            int32_t store_f64, VegsSplatTable *out, void *stream);
+
+/* Splat table from already-projected splats (the reference's SplatData, pipeline.py:40-49):
+ * m rows of float64 mean2d (m x 2), conic (m x 3), alpha_base, depth, channels (m x C) and
+ * int32 rect (m x 4).  Every row counts as kept.  Same record / key layout as above. */
+int vegs_splat_table_from_arrays(const double *mean2d, const double *conic, const double *alpha_base,
+                                 const double *depth, const int32_t *rect, const double *channels,
+                                 int64_t m, const VegsSettings *st, int32_t n_channels, int32_t store_f64,
+                                 VegsSplatTable *out, void *stream);
+
+/* ---- binning ---------------------------------------------------------------------- */
+/* Scan of (kept, tiles): offsets[n+1] (instance offset per Gaussian, duplicate order),
+ * kept_idx[n+1] (index in the kept list), counts[2] = {n_kept, n_instances} (device). */
+int vegs_bin_count(const uint32_t *tiles, int64_t n, int64_t *offsets, int64_t *kept_idx,
+                   int64_t *counts, void *ws, size_t *ws_bytes, void *stream);
+
+/* Duplicate + radix sort on (tile, depth rank) == np.lexsort((depth, tile)).
+ * Outputs (n_inst): sorted_gauss (Gaussian id), inst_pid (duplicate-order index),
+ * order (kept index, the reference's `order`; may be NULL); tile_start/tile_end (n_tiles). */
+int vegs_bin_sort(const uint32_t *tiles, const uint64_t *depth_key, const int32_t *rect,
+                  const int64_t *offsets, const int64_t *kept_idx, int64_t n, int64_t n_kept,
+                  int64_t n_inst, int32_t width, int32_t height, int32_t tile_size,
+                  uint32_t *sorted_gauss, uint32_t *inst_pid, int64_t *order,
+                  int32_t *tile_start, int32_t *tile_end, void *ws, size_t *ws_bytes,
+                  void *stream);
+
+/* ---- composite -------------------------------------------------------------------- */
+/* Tile blend on the splat table.  out_img H x W x C, out_t H x W (storage type),
+ * out_last H x W int32 (sorted-instance index, -1 = none), n_contrib H x W int32. */
+int vegs_composite_forward(const int32_t *tile_start, const int32_t *tile_end,
+                           const uint32_t *sorted_gauss, const void *record, const int32_t *rect,
+                           int32_t n_channels, int32_t store_f64, const double *bg, int32_t width,
+                           int32_t height, double alpha_clamp, double trans_stop, void *out_img,
+                           void *out_t, int32_t *out_last, int32_t *n_contrib, void *stream);
+
+/* Backward tile blend.  d_img H x W x C, d_alpha H x W (storage type).  Writes per-
+ * instance rows [g_mx, g_my, g_ca, g_cb, g_cc, g_alpha, g_ch...] (row stride rec_stride)
+ * at the instance's duplicate-order index inst_pid[s]. */
+int vegs_composite_backward(const int32_t *tile_start, const int32_t *tile_end,
+                            const uint32_t *sorted_gauss, const uint32_t *inst_pid,
+                            const void *record, const int32_t *rect, int32_t n_channels,
+                            int32_t store_f64, const double *bg, int32_t width, int32_t height,
+                            double alpha_clamp, const void *out_t, const int32_t *out_last,
+                            const void *d_img, const void *d_alpha, void *inst_rows, void *stream);
+
+/* Per-Gaussian: float64 reduction of its instance rows (duplicate order == np.add.at
+ * order), then projection and shading backward.  grads: flat float64 class-major
+ * buffer (19 n); grads = accumulate ? grads + scale * g : scale * g.  viewspace_norm /
+ * visible may be NULL. */
+int vegs_preprocess_backward(const double *params, int64_t n, const VegsCamera *cam,
+                             const VegsTF *tf, const VegsSettings *st, int32_t n_channels,
+                             int32_t store_f64, const uint32_t *tiles, const int64_t *offsets,
+                             const void *inst_rows, double scale, int32_t accumulate,
+                             double *grads, double *viewspace_norm, uint8_t *visible,
+                             void *stream);
+
+/* ---- drop-in raw kernels (reference argument lists) -------------------------------- */
+int vegs_blend_forward(const int64_t *tile_start, const int64_t *tile_end, int64_t n_tiles,
+                       int64_t tiles_x, int64_t tile_size, const void *inst_mean2d,
+                       const void *inst_conic, const void *inst_alpha, const void *inst_pmin,
+                       const int32_t *inst_rect, const void *inst_channels, int32_t n_channels,
+                       int32_t store_f64, const void *bg, int64_t width, int64_t height,
+                       double alpha_clamp, double trans_stop, void *out_img, void *out_t,
+                       int64_t *out_last, int32_t *n_contrib, void *stream);
+
+int vegs_blend_backward(const int64_t *tile_start, const int64_t *tile_end, int64_t n_tiles,
+                        int64_t tiles_x, int64_t tile_size, const void *inst_mean2d,
+                        const void *inst_conic, const void *inst_alpha, const void *inst_pmin,
+                        const int32_t *inst_rect, const void *inst_channels, int32_t n_channels,
+                        int32_t store_f64, const void *bg, int64_t width, int64_t height,
+                        double alpha_clamp, const void *out_t, const int64_t *out_last,
+                        const void *d_img, const void *d_alpha_plane, void *g_mean2d,
+                        void *g_conic, void *g_alpha, void *g_channels, void *stream);
+
+/* ---- loss / optimiser ------------------------------------------------------------- */
+/* (w_l1) * mean|x - y| + lam * (1 - mean SSIM) on H x W x 3 float32 images; writes
+ * d_x (H x W x 3 float32) and accumulates {sum |x-y|, sum ssim_map} into sums[2]
+ * (float64, caller zeroes).  ws holds the SSIM gradient maps. */
+int vegs_loss_l1_ssim(const float *x, const float *y, int32_t height, int32_t width,
+                      double w_l1, double lam, float *d_x, double *sums, void *ws,
+                      size_t *ws_bytes, void *stream);
+
+/* In-place bias-corrected Adam over the flat class-major float64 buffers (19 n).
+ * lr[10] per class, grad_scale multiplies g first, bias1/bias2 = 1 - beta^t.
+ * nonfinite[10] (int32) receives 1 for classes that saw a non-finite gradient. */
+int vegs_adam_step(double *params, const double *grads, double *m, double *v, int64_t n,
+                   const double *lr, double grad_scale, double bias1, double bias2,
+                   int32_t *nonfinite, void *stream);
+
+/* Library build identity (for the loader's sanity check). */
+const char *vegs_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* VEGSPLAT_B200_H */

@@ -1,0 +1,350 @@
+"""Device-side orchestration of the rasteriser: torch tensors own HBM, the C-ABI does the work.
+
+Per view, the forward pipeline is five launches on the current CUDA stream:
+
+    vegs_preprocess_forward  per-Gaussian TF + shading + EWA projection -> splat table
+    vegs_bin_count           scan of (kept, tiles touched)        [one 16-byte readback]
+    vegs_bin_sort            depth rank, duplication, (tile, rank) radix sort, ranges
+    vegs_composite_forward   tile blend -> image, T, last contributor, contributor count
+
+and the backward is two more (``vegs_composite_backward`` -> per-instance rows,
+``vegs_preprocess_backward`` -> float64 per-Gaussian gradients).  The only host
+synchronisation is the instance count needed to size the sort.
+
+Nothing here computes on the CPU: if CUDA or the library is missing, ``require_cuda``
+raises.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import _lib
+from ._lib import VegsCamera, VegsError, VegsSettings, VegsSplatTable, VegsTF, call
+from .constants import DEFAULT_SETTINGS, RasterSettings
+from .transfer import TransferFunction, pack_tf
+
+TILE = 16
+
+# Kernels launched per C-ABI call (our kernels plus the CUB kernels instantiated inside
+# libvegsplat_b200.so); checked against the ncu launch list in profiles/.
+LAUNCHES = {
+    "vegs_preprocess_forward": 1,
+    "vegs_splat_table_from_arrays": 1,
+    "vegs_bin_count": 4,          # pack, CUB scan (init + sweep), unpack
+    "vegs_bin_sort": 20,          # iota, CUB depth sort (hist + scan + 8 onesweep), rank, duplicate,
+                                  # CUB key sort (hist + scan + 4 onesweep), finalize
+    "vegs_composite_forward": 1,
+    "vegs_composite_backward": 1,
+    "vegs_preprocess_backward": 1,
+    "vegs_loss_l1_ssim": 2,
+    "vegs_adam_step": 1,
+}
+
+
+def require_cuda() -> torch.device:
+    if not torch.cuda.is_available():
+        raise VegsError("vegsplat_b200 needs a CUDA device (B200): there is no CPU path")
+    _lib.load()
+    return torch.device("cuda", torch.cuda.current_device())
+
+
+def _p(t: torch.Tensor | None):
+    return None if t is None else ctypes.c_void_p(t.data_ptr())
+
+
+def _stream():
+    return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def rec_stride(n_ch: int) -> int:
+    return ((7 + n_ch) + 3) & ~3
+
+
+def camera_struct(cam) -> VegsCamera:
+    c = VegsCamera()
+    c.position[:] = [float(x) for x in cam.position]
+    rot = np.asarray(cam.world_to_cam_rotation(), dtype=np.float64).ravel()
+    c.rot[:] = rot.tolist()
+    tan_y = math.tan(0.5 * cam.fov_y)
+    c.focal = 0.5 * cam.height / tan_y
+    c.tan_y = tan_y
+    c.tan_x = tan_y * (cam.width / cam.height)
+    c.near_z = float(cam.near)
+    c.width, c.height = int(cam.width), int(cam.height)
+    return c
+
+
+def settings_struct(s: RasterSettings) -> VegsSettings:
+    if s.tile_size != TILE:
+        raise ValueError(f"tile_size {s.tile_size} unsupported: the B200 kernels use 16x16 tiles")
+    v = VegsSettings()
+    v.dilation, v.alpha_clamp, v.alpha_skip = s.dilation, s.alpha_clamp, s.alpha_skip
+    v.transmittance_stop, v.radius_sigma, v.rect_margin_px = s.transmittance_stop, s.radius_sigma, s.rect_margin_px
+    v.cull_alpha, v.frustum_limit, v.tile_size = s.cull_alpha, s.frustum_limit, s.tile_size
+    return v
+
+
+class DeviceTF:
+    """Transfer-function knot tables resident in HBM (staged to SMEM by the kernels)."""
+
+    def __init__(self, tf: TransferFunction, device=None):
+        blob, k_op, k_col = pack_tf(tf)
+        self.tf = tf
+        self.blob = torch.from_numpy(blob).to(device or require_cuda())
+        self.struct = VegsTF(ctypes.c_void_p(self.blob.data_ptr()), k_op, k_col)
+
+
+class Pool:
+    """Grow-only scratch buffers keyed by name (reused across views of a step)."""
+
+    def __init__(self, device):
+        self.device = device
+        self.bufs: dict[str, torch.Tensor] = {}
+
+    def get(self, name: str, numel: int, dtype) -> torch.Tensor:
+        numel = max(int(numel), 1)
+        t = self.bufs.get(name)
+        if t is None or t.numel() < numel or t.dtype != dtype:
+            t = torch.empty(int(numel * 1.1) + 64 if t is not None else numel, dtype=dtype, device=self.device)
+            self.bufs[name] = t
+        return t[:numel]
+
+
+class _Fresh:
+    def __init__(self, device):
+        self.device = device
+
+    def get(self, name: str, numel: int, dtype) -> torch.Tensor:
+        return torch.empty(max(int(numel), 1), dtype=dtype, device=self.device)
+
+
+@dataclass
+class Frame:
+    """Everything one forward leaves on the device for its backward."""
+
+    n: int
+    n_ch: int
+    store_f64: bool
+    width: int
+    height: int
+    cam: VegsCamera | None
+    tf: DeviceTF | None
+    settings: VegsSettings
+    bg: ctypes.Array
+    params: torch.Tensor | None
+    record: torch.Tensor
+    rect: torch.Tensor
+    tiles: torch.Tensor
+    depth_key: torch.Tensor
+    offsets: torch.Tensor
+    kept_idx: torch.Tensor
+    n_kept: int
+    n_inst: int
+    sorted_gauss: torch.Tensor
+    inst_pid: torch.Tensor
+    order: torch.Tensor | None
+    tile_start: torch.Tensor
+    tile_end: torch.Tensor
+    out_img: torch.Tensor
+    out_t: torch.Tensor
+    out_last: torch.Tensor
+    n_contrib: torch.Tensor
+    api: dict = field(default_factory=dict)
+
+    @property
+    def real(self):
+        return torch.float64 if self.store_f64 else torch.float32
+
+
+class Rasterizer:
+    """Forward / backward of the tile rasteriser on the current CUDA stream.
+
+    ``pooled=True`` reuses scratch between calls (training loops: forward, loss and
+    backward of one view complete before the next view starts); ``pooled=False``
+    gives every Frame its own buffers (the reference-shaped API, where a RenderState
+    may outlive later renders)."""
+
+    def __init__(self, settings: RasterSettings = DEFAULT_SETTINGS, n_channels: int = 3,
+                 store_f64: bool = False, pooled: bool = True):
+        if n_channels not in (3, 11):
+            raise ValueError("n_channels must be 3 (rgb) or 11 (rgb + aux planes)")
+        self.device = require_cuda()
+        self.settings = settings
+        self.st = settings_struct(settings)
+        self.n_ch = n_channels
+        self.store_f64 = store_f64
+        self.real = torch.float64 if store_f64 else torch.float32
+        self.pool = Pool(self.device) if pooled else None
+        self.timer = None  # optional KernelTimer: CUDA events around each launch group
+        self.launches = 0  # kernels launched by this rasteriser (see LAUNCHES)
+        self.last_counts = (0, 0)  # (kept splats, tile instances) of the latest forward
+
+    def _run(self, name: str, *args) -> None:
+        if self.timer is not None:
+            self.timer.mark(name, True)
+        call(name, *args)
+        if self.timer is not None:
+            self.timer.mark(name, False)
+        self.launches += LAUNCHES.get(name, 1)
+
+    def _alloc(self):
+        return self.pool if self.pool is not None else _Fresh(self.device)
+
+    # -- forward --------------------------------------------------------------------
+    def forward(self, params: torch.Tensor, n: int, tf: DeviceTF, cam, background=(1.0, 1.0, 1.0),
+                want_order: bool = False, api_views: bool = False) -> Frame:
+        A = self._alloc()
+        rs = rec_stride(self.n_ch)
+        record = A.get("record", n * rs, self.real)
+        rect = A.get("rect", n * 4, torch.int32)
+        tiles = A.get("tiles", n, torch.int32)
+        depth_key = A.get("depth_key", n, torch.int64)
+        tab = VegsSplatTable(_p(record), _p(rect), _p(tiles), _p(depth_key))
+        api = {}
+        if api_views:
+            api = dict(mean2d=A.get("a_mean2d", 2 * n, torch.float64), conic=A.get("a_conic", 3 * n, torch.float64),
+                       depth=A.get("a_depth", n, torch.float64), alpha_base=A.get("a_ab", n, torch.float64),
+                       color=A.get("a_color", 3 * n, torch.float64), radius=A.get("a_radius", n, torch.float64),
+                       visible=A.get("a_visible", n, torch.uint8), aux=A.get("a_aux", 24 * n, torch.float64))
+            for k, v in api.items():
+                setattr(tab, k, _p(v))
+        cs = camera_struct(cam)
+        self._run("vegs_preprocess_forward", _p(params), n, ctypes.byref(cs), ctypes.byref(tf.struct),
+             ctypes.byref(self.st), self.n_ch, int(self.store_f64), ctypes.byref(tab), _stream())
+        return self._bin_and_blend(A, n, record, rect, tiles, depth_key, cam.width, cam.height, background,
+                                   cs, tf, params, want_order, api)
+
+    def forward_from_splats(self, mean2d, conic, alpha_base, depth, rect, channels, width, height,
+                            background, want_order: bool = True) -> Frame:
+        """rasterize_forward on already-projected splats (pipeline.py:197-237)."""
+        A = self._alloc()
+        m = int(alpha_base.shape[0])
+        rs = rec_stride(self.n_ch)
+        record = A.get("record", m * rs, self.real)
+        rect_d = A.get("rect", m * 4, torch.int32)
+        tiles = A.get("tiles", m, torch.int32)
+        depth_key = A.get("depth_key", m, torch.int64)
+        tab = VegsSplatTable(_p(record), _p(rect_d), _p(tiles), _p(depth_key))
+        self._run("vegs_splat_table_from_arrays", _p(mean2d), _p(conic), _p(alpha_base), _p(depth), _p(rect),
+             _p(channels), m, ctypes.byref(self.st), self.n_ch, int(self.store_f64), ctypes.byref(tab), _stream())
+        return self._bin_and_blend(A, m, record, rect_d, tiles, depth_key, width, height, background, None,
+                                   None, None, want_order, {})
+
+    def _bin_and_blend(self, A, n, record, rect, tiles, depth_key, width, height, background, cs, tf, params,
+                       want_order, api) -> Frame:
+        offsets = A.get("offsets", n + 1, torch.int64)
+        kept_idx = A.get("kept_idx", n + 1, torch.int64)
+        counts = A.get("counts", 2, torch.int64)
+        s = _stream()
+        wsz = _lib.size_query("vegs_bin_count", _p(tiles), n, _p(offsets), _p(kept_idx), _p(counts), tail=(s,))
+        ws = A.get("ws_count", wsz, torch.uint8)
+        self._run("vegs_bin_count", _p(tiles), n, _p(offsets), _p(kept_idx), _p(counts), _p(ws),
+             ctypes.byref(ctypes.c_size_t(wsz)), s)
+        n_kept, n_inst = (int(x) for x in counts.tolist())  # the one host sync per view
+        self.last_counts = (n_kept, n_inst)
+        tiles_x = (width + TILE - 1) // TILE
+        n_tiles = tiles_x * ((height + TILE - 1) // TILE)
+        sorted_gauss = A.get("sorted_gauss", n_inst, torch.int32)
+        inst_pid = A.get("inst_pid", n_inst, torch.int32)
+        order = A.get("order", n_inst, torch.int64) if want_order else None
+        tile_start = A.get("tile_start", n_tiles, torch.int32)
+        tile_end = A.get("tile_end", n_tiles, torch.int32)
+        args = (_p(tiles), _p(depth_key), _p(rect), _p(offsets), _p(kept_idx), n, n_kept, n_inst, width, height,
+                TILE, _p(sorted_gauss), _p(inst_pid), _p(order), _p(tile_start), _p(tile_end))
+        wsz = _lib.size_query("vegs_bin_sort", *args, tail=(s,))
+        ws = A.get("ws_sort", wsz, torch.uint8)
+        self._run("vegs_bin_sort", *args, _p(ws), ctypes.byref(ctypes.c_size_t(wsz)), s)
+        hw = width * height
+        out_img = A.get("out_img", hw * self.n_ch, self.real)
+        out_t = A.get("out_t", hw, self.real)
+        out_last = A.get("out_last", hw, torch.int32)
+        n_contrib = A.get("n_contrib", hw, torch.int32)
+        bg = (ctypes.c_double * 3)(*[float(x) for x in background])
+        self._run("vegs_composite_forward", _p(tile_start), _p(tile_end), _p(sorted_gauss), _p(record), _p(rect),
+             self.n_ch, int(self.store_f64), bg, width, height, float(self.settings.alpha_clamp),
+             float(self.settings.transmittance_stop), _p(out_img), _p(out_t), _p(out_last), _p(n_contrib), s)
+        return Frame(n=n, n_ch=self.n_ch, store_f64=self.store_f64, width=width, height=height, cam=cs, tf=tf,
+                     settings=self.st, bg=bg, params=params, record=record, rect=rect, tiles=tiles,
+                     depth_key=depth_key, offsets=offsets, kept_idx=kept_idx, n_kept=n_kept, n_inst=n_inst,
+                     sorted_gauss=sorted_gauss, inst_pid=inst_pid, order=order, tile_start=tile_start,
+                     tile_end=tile_end, out_img=out_img, out_t=out_t, out_last=out_last, n_contrib=n_contrib,
+                     api=api)
+
+    # -- backward -------------------------------------------------------------------
+    def backward_rows(self, fr: Frame, d_img: torch.Tensor, d_alpha: torch.Tensor | None = None) -> torch.Tensor:
+        """Per-instance gradient rows (duplicate order) from the backward tile blend."""
+        A = self._alloc()
+        rs = rec_stride(fr.n_ch)
+        rows = A.get("rows", max(fr.n_inst, 1) * rs, fr.real)
+        if d_alpha is None:
+            d_alpha = A.get("zero_alpha", fr.width * fr.height, fr.real)
+            d_alpha.zero_()
+        d_img, d_alpha = d_img.contiguous(), d_alpha.contiguous()  # referenced until enqueued
+        self._run("vegs_composite_backward", _p(fr.tile_start), _p(fr.tile_end), _p(fr.sorted_gauss), _p(fr.inst_pid),
+             _p(fr.record), _p(fr.rect), fr.n_ch, int(fr.store_f64), fr.bg, fr.width, fr.height,
+             float(self.settings.alpha_clamp), _p(fr.out_t), _p(fr.out_last), _p(d_img),
+             _p(d_alpha), _p(rows), _stream())
+        return rows
+
+    def backward(self, fr: Frame, d_img: torch.Tensor, d_alpha: torch.Tensor | None = None,
+                 grads: torch.Tensor | None = None, scale: float = 1.0, accumulate: bool = False,
+                 viewspace_norm: torch.Tensor | None = None, visible: torch.Tensor | None = None) -> torch.Tensor:
+        """Full analytic backward into the flat float64 gradient buffer (19 n)."""
+        if fr.params is None:
+            raise ValueError("backward through the full chain needs a Frame from forward()")
+        rows = self.backward_rows(fr, d_img, d_alpha)
+        if grads is None:
+            grads = torch.empty(19 * fr.n, dtype=torch.float64, device=self.device)
+        self._run("vegs_preprocess_backward", _p(fr.params), fr.n, ctypes.byref(fr.cam), ctypes.byref(fr.tf.struct),
+             ctypes.byref(fr.settings), fr.n_ch, int(fr.store_f64), _p(fr.tiles), _p(fr.offsets), _p(rows),
+             float(scale), int(accumulate), _p(grads), _p(viewspace_norm), _p(visible), _stream())
+        return grads
+
+
+# -- small device utilities -------------------------------------------------------------
+
+def tf_eval(ts, vals, v, derivative: bool) -> np.ndarray:
+    """Device TF lookup (interp or half-open slope) for host arrays; returns (..., n_cols)."""
+    dev = require_cuda()
+    ts = np.ascontiguousarray(ts, dtype=np.float64)
+    vals = np.asarray(vals, dtype=np.float64)
+    q = np.asarray(v, dtype=np.float64)
+    shape = q.shape
+    cols = vals.shape[1]
+    ts_d = torch.from_numpy(ts).to(dev)
+    vals_d = torch.from_numpy(np.ascontiguousarray(vals.T)).to(dev)  # column-major
+    q_d = torch.from_numpy(np.ascontiguousarray(q.ravel())).to(dev)
+    out = torch.empty(q_d.numel() * cols, dtype=torch.float64, device=dev)
+    call("vegs_tf_eval", _p(ts_d), _p(vals_d), len(ts), cols, _p(q_d), q_d.numel(), int(derivative), _p(out),
+         _stream())
+    return out.cpu().numpy().reshape(shape + (cols,))
+
+
+class LossKernel:
+    """Fused L1 + SSIM forward/backward (vegs_loss_l1_ssim) with a reusable workspace."""
+
+    def __init__(self, device=None):
+        self.device = device or require_cuda()
+        self.pool = Pool(self.device)
+
+    def __call__(self, x: torch.Tensor, y: torch.Tensor, w_l1: float, lam: float, d_x: torch.Tensor,
+                 sums: torch.Tensor) -> None:
+        h, w = int(x.shape[0]), int(x.shape[1])
+        nbytes = _lib.size_query("vegs_loss_l1_ssim", _p(x), _p(y), h, w, float(w_l1), float(lam), _p(d_x),
+                                 _p(sums), tail=(_stream(),))
+        ws = self.pool.get("ws", nbytes, torch.uint8)
+        call("vegs_loss_l1_ssim", _p(x), _p(y), h, w, float(w_l1), float(lam), _p(d_x), _p(sums), _p(ws),
+             ctypes.byref(ctypes.c_size_t(nbytes)), _stream())
+
+
+def adam_step_device(params, grads, m, v, n: int, lrs: torch.Tensor, grad_scale: float, step: int,
+                     nonfinite: torch.Tensor) -> None:
+    b1, b2 = 0.9, 0.999
+    call("vegs_adam_step", _p(params), _p(grads), _p(m), _p(v), n, _p(lrs), float(grad_scale),
+         1.0 - b1 ** step, 1.0 - b2 ** step, _p(nonfinite), _stream())

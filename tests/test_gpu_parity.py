@@ -1,0 +1,329 @@
+"""CUDA path vs the reference (golden vectors) and vs the CPU oracle, through the C-ABI.
+
+Bars (BASELINE.json north star):
+  * integer outputs bit-exact: kept set, rects, instance order, tile ranges, last
+    contributor per pixel, contributor count per pixel;
+  * images: |gpu - ref| <= 1e-4 * max(|ref|, 1e-3) per pixel (float32 blends);
+  * gradients: ||gpu - ref||_inf <= 1e-4 * ||ref||_inf per parameter class (float32
+    blends; the float64 blend path is held to 1e-9).
+"""
+
+import math
+
+import numpy as np
+import pytest
+
+import goldens as G
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():  # the gpu marker is deselected on CPU runs anyway
+    pytest.skip("needs CUDA", allow_module_level=True)
+
+from oracle import vegs_oracle as O  # noqa: E402
+from paper_2504_13339_b200 import raster as R  # noqa: E402
+from paper_2504_13339_b200.constants import DEFAULT_SETTINGS as S  # noqa: E402
+
+IMG_REL = 1e-4
+GRAD_REL_F32 = 1e-4
+GRAD_REL_F64 = 1e-9
+
+
+def img_close(a, b, rel=IMG_REL):
+    a = np.asarray(a, dtype=np.float64)
+    b = np.asarray(b, dtype=np.float64)
+    return bool(np.all(np.abs(a - b) <= rel * np.maximum(np.abs(b), 1e-3)))
+
+
+FWD = [("c0_f32", np.float32, False), ("c0_f64", np.float64, False),
+       ("c0_aux_f32", np.float32, True), ("dense_f32", np.float32, False)]
+
+
+@pytest.fixture(scope="module", params=FWD, ids=[f[0] for f in FWD])
+def golden_case(request):
+    name, dt, aux = request.param
+    d = G.load(name)
+    img, st = R.render_with_state(G.gs_of(d), G.tf_of(d), G.cam_of(d["cam"]), tuple(d["bg"]), S, aux, dt)
+    return name, dt, aux, d, img, st
+
+
+def test_golden_integer_outputs_bit_exact(golden_case):
+    name, dt, aux, d, img, st = golden_case
+    b = st.blend
+    assert np.array_equal(st.kept, d["kept"])
+    assert np.array_equal(st.proj.rect, d["rect"])
+    assert np.array_equal(b.order, d["order"])
+    assert np.array_equal(b.tile_start, d["tile_start"])
+    assert np.array_equal(b.tile_end, d["tile_end"])
+    assert np.array_equal(b.out_last, d["out_last"])
+    assert np.array_equal(b.n_contrib, d["n_contrib"])
+
+
+def test_golden_blend_inputs_and_planes(golden_case):
+    name, dt, aux, d, img, st = golden_case
+    b = st.blend
+    assert np.array_equal(st.proj.depth, d["depth"]) or np.abs(st.proj.depth - d["depth"]).max() < 1e-14
+    assert np.abs(b.inst_pmin.astype(np.float64) - d["inst_pmin"]).max() <= 1e-6
+    assert img_close(b.out_t, d["out_t"])
+    assert img_close(img.rgb, d["rgb"])
+    assert img_close(img.alpha, d["alpha"], rel=1e-3)
+    if dt == np.float32:  # T is reproduced bit for bit
+        assert np.array_equal(b.out_t, d["out_t"])
+    if aux:
+        assert img_close(img.depth, d["depth_plane"])
+        assert img_close(img.normal, d["normal_plane"])
+        assert img_close(img.attrs, d["attrs_plane"])
+
+
+def test_golden_gradients(golden_case):
+    name, dt, aux, d, img, st = golden_case
+    kw = {k: d["probe_" + k] for k in ("rgb", "alpha", "depth", "normal", "attrs") if "probe_" + k in d}
+    g = R.rasterize_backward(st, R.ImageGradients(**kw))
+    tol = GRAD_REL_F32 if dt == np.float32 else GRAD_REL_F64
+    for k in O.GRAD_CLASSES:
+        assert G.norm_rel(getattr(g, k), d["grad_" + k]) <= tol, (k, G.norm_rel(getattr(g, k), d["grad_" + k]))
+    assert np.array_equal(g.visible, d["grad_visible"])
+    assert G.norm_rel(g.viewspace_norm, d["grad_viewspace_norm"]) <= tol
+
+
+def test_backward_is_deterministic():
+    d = G.load("c0_f32")
+    out = []
+    for _ in range(2):
+        img, st = R.render_with_state(G.gs_of(d), G.tf_of(d), G.cam_of(d["cam"]), tuple(d["bg"]), S, False,
+                                      np.float32)
+        g = R.rasterize_backward(st, R.ImageGradients(rgb=d["probe_rgb"], alpha=d["probe_alpha"]))
+        out.append(g)
+    for k in O.GRAD_CLASSES:
+        assert np.array_equal(getattr(out[0], k), getattr(out[1], k)), k
+
+
+@pytest.mark.parametrize("seed", range(8))
+def test_reference_gradcheck_scenes(seed):
+    d = G.load("gradcheck_scenes")
+    p = f"s{seed}_"
+    img, st = R.render_with_state(G.gs_of(d, p + "gs_"), G.tf_of(d, p + "tf_"), G.cam_of(d[p + "cam"]),
+                                  tuple(d[p + "bg"]), S, True, np.float64)
+    assert np.abs(img.rgb - d[p + "rgb"]).max() < 1e-12
+    assert np.abs(img.depth - d[p + "depth_plane"]).max() < 1e-12
+    g = R.rasterize_backward(st, R.ImageGradients(**{k: d[p + "probe_" + k]
+                                                     for k in ("rgb", "alpha", "depth", "normal", "attrs")}))
+    for k in O.GRAD_CLASSES:
+        assert G.norm_rel(getattr(g, k), d[p + "grad_" + k]) <= 1e-9, k
+
+
+@pytest.mark.parametrize("seed", range(5))
+def test_rasterize_forward_on_reference_splats(seed):
+    d = G.load("blend_scenes")
+    p = f"s{seed}_"
+    data = R.SplatData(**{k: d[p + k] for k in ("mean2d", "conic", "alpha_base", "depth", "rect", "channels")})
+    w, h = (int(x) for x in d[p + "wh"])
+    img, b = R.rasterize_forward(data, w, h, d[p + "bg"], S)
+    assert np.array_equal(b.order, d[p + "order"])
+    assert np.array_equal(b.out_last, d[p + "out_last"])
+    assert np.abs(img.rgb - d[p + "rgb"]).max() < 1e-12
+
+
+# -- known-answer tests (reference tests/test_rasterize.py:35-63) ----------------------
+
+def _splats(mean2d, conic, alpha, depth, rect, ch):
+    return R.SplatData(mean2d=np.array(mean2d, dtype=float), conic=np.array(conic, dtype=float),
+                       alpha_base=np.array(alpha, dtype=float), depth=np.array(depth, dtype=float),
+                       rect=np.array(rect, dtype=np.int32).reshape(-1, 4), channels=np.array(ch, dtype=float))
+
+
+def test_kat_zero_splats_is_background():
+    data = _splats(np.zeros((0, 2)), np.zeros((0, 3)), [], [], np.zeros((0, 4)), np.zeros((0, 3)))
+    img, _ = R.rasterize_forward(data, 32, 32, (0.1, 0.2, 0.3))
+    assert np.allclose(img.rgb, [0.1, 0.2, 0.3])
+    assert np.allclose(img.alpha, 0.0)
+
+
+def test_kat_single_centered_splat():
+    data = _splats([[16.5, 16.5]], [[1.0, 0.0, 1.0]], [0.5], [1.0], [0, 32, 0, 32], [[1.0, 0.0, 0.0]])
+    img, _ = R.rasterize_forward(data, 32, 32, (0.0, 0.0, 1.0))
+    assert np.allclose(img.rgb[16, 16], [0.5, 0.0, 0.5], atol=1e-12)
+    assert img.alpha[16, 16] == pytest.approx(0.5)
+
+
+def test_kat_two_coincident_splats():
+    data = _splats([[16.5, 16.5]] * 2, [[1.0, 0.0, 1.0]] * 2, [0.5, 0.5], [1.0, 2.0],
+                   [[0, 32, 0, 32], [0, 32, 0, 32]], [[1.0, 0.0, 0.0], [0.0, 1.0, 0.0]])
+    img, _ = R.rasterize_forward(data, 32, 32, (0.0, 0.0, 1.0))
+    assert np.allclose(img.rgb[16, 16], [0.5, 0.25, 0.25], atol=1e-12)
+
+
+# -- the drop-in raw kernels on the reference's instance arrays -------------------------
+
+def test_raw_blend_kernels_match_oracle():
+    from paper_2504_13339_b200 import kernels as K
+
+    d = G.load("dense_f32")
+    img_o, st = O.render_with_state(G.gs_of(d), G.tf_of(d), G.cam_of(d["cam"]), tuple(d["bg"]), S, False,
+                                    np.float32)
+    h, w = st["height"], st["width"]
+    out_img = np.zeros((h, w, 3), np.float32)
+    out_t = np.ones((h, w), np.float32)
+    out_last = np.full((h, w), -1, np.int64)
+    ncon = np.zeros((h, w), np.int32)
+    K.blend_forward(st["tile_start"], st["tile_end"], st["tiles_x"], 16, st["inst_mean2d"], st["inst_conic"],
+                    st["inst_alpha"], st["inst_pmin"], st["inst_rect"], st["inst_channels"], st["bg"], w, h,
+                    np.float32(0.99), np.float32(1e-4), out_img, out_t, out_last, ncon)
+    assert np.array_equal(out_last, st["out_last"])
+    assert np.array_equal(ncon, st["n_contrib"])
+    assert np.array_equal(out_t, st["out_t"])
+    assert img_close(out_img, st["out_img"])
+    n = len(st["order"])
+    g = [np.zeros((n, 2), np.float32), np.zeros((n, 3), np.float32), np.zeros(n, np.float32),
+         np.zeros((n, 3), np.float32)]
+    K.blend_backward(st["tile_start"], st["tile_end"], st["tiles_x"], 16, st["inst_mean2d"], st["inst_conic"],
+                     st["inst_alpha"], st["inst_pmin"], st["inst_rect"], st["inst_channels"], st["bg"], w, h,
+                     np.float32(0.99), st["out_t"], st["out_last"], d["probe_rgb"].astype(np.float32),
+                     d["probe_alpha"].astype(np.float32), *g)
+    ref = O.blend_backward(st, d["probe_rgb"], d["probe_alpha"])
+    for mine, k in zip(g, ("mean2d", "conic", "alpha", "channels")):
+        assert G.norm_rel(mine, ref[k]) <= GRAD_REL_F32, k
+
+
+# -- larger scale vs the oracle (config 1 geometry: 100k Gaussians, 512 x 512) -----------
+
+@pytest.fixture(scope="module")
+def c1_case():
+    from paper_2504_13339_b200 import scenes
+
+    gs, _, tf, cams = scenes.config_scene("c1")
+    cam = cams[0]
+    img_o, st_o = O.render_with_state(gs, tf, cam, (1.0, 1.0, 1.0), S, False, np.float32)
+    img_g, st_g = R.render_with_state(gs, tf, cam, (1.0, 1.0, 1.0), S, False, np.float32)
+    return gs, tf, cam, img_o, st_o, img_g, st_g
+
+
+def test_c1_forward_vs_oracle(c1_case):
+    gs, tf, cam, img_o, st_o, img_g, st_g = c1_case
+    b = st_g.blend
+    assert np.array_equal(st_g.kept, st_o["kept"])
+    assert np.array_equal(st_g.proj.rect, st_o["proj"]["rect"])
+    assert np.array_equal(b.order, st_o["order"])
+    assert np.array_equal(b.tile_start, st_o["tile_start"]) and np.array_equal(b.tile_end, st_o["tile_end"])
+    assert np.array_equal(b.out_last, st_o["out_last"])
+    assert np.array_equal(b.n_contrib, st_o["n_contrib"])
+    assert img_close(img_g.rgb, img_o["rgb"])
+    assert img_close(b.out_t, st_o["out_t"])
+
+
+def test_c1_backward_vs_oracle(c1_case):
+    gs, tf, cam, img_o, st_o, img_g, st_g = c1_case
+    rng = np.random.default_rng(5)
+    d_rgb = rng.uniform(-1, 1, size=(cam.height, cam.width, 3))
+    g_o = O.rasterize_backward(st_o, d_rgb)
+    g_g = R.rasterize_backward(st_g, R.ImageGradients(rgb=d_rgb))
+    for k in O.GRAD_CLASSES:
+        assert G.norm_rel(getattr(g_g, k), g_o[k]) <= GRAD_REL_F32, k
+
+
+# -- TF lookup, loss, Adam --------------------------------------------------------------
+
+def test_tf_lookup_bitwise_vs_numpy():
+    from paper_2504_13339_b200 import device
+
+    d = G.load("tf_lookup")
+    for j in range(5):
+        ts, q = d[f"k{j}_ts"], d[f"k{j}_q"]
+        assert np.array_equal(device.tf_eval(ts, d[f"k{j}_op"][:, None], q, False)[:, 0], d[f"k{j}_eval_op"])
+        assert np.array_equal(device.tf_eval(ts, d[f"k{j}_col"], q, False), d[f"k{j}_eval_col"])
+        assert np.array_equal(device.tf_eval(ts, d[f"k{j}_op"][:, None], q, True)[:, 0], d[f"k{j}_d_op"])
+        assert np.array_equal(device.tf_eval(ts, d[f"k{j}_col"], q, True), d[f"k{j}_d_col"])
+
+
+def test_loss_vs_reference():
+    from paper_2504_13339_b200.images import ImageBuffer
+    from paper_2504_13339_b200.loss import compute_loss
+
+    class Cfg:
+        lambda_ssim = 0.2
+        normal_loss_weight = 0.0
+        smooth_loss_weight = 0.0
+
+    d = G.load("loss")
+    total, grads, br = compute_loss(ImageBuffer(rgb=d["f32_x"]), d["f32_y"], Cfg())
+    assert abs(total - float(d["f32_total"])) <= 1e-5 * abs(float(d["f32_total"]))
+    assert abs((1 - br.ssim_term) - float(d["f32_ssim"])) <= 1e-5
+    assert G.norm_rel(grads.rgb, d["f32_grad"]) <= 1e-4
+
+
+def test_adam_matches_reference_bitwise():
+    from paper_2504_13339_b200.model import GaussianSet, PARAM_CLASSES
+    from paper_2504_13339_b200.raster import GradientSet
+    from paper_2504_13339_b200.train import OptimizerState, TrainConfig, adam_step
+
+    d = G.load("adam")
+    gs = GaussianSet(**{k: d["in_" + k].copy() for k in PARAM_CLASSES})
+    opt = OptimizerState.for_set(gs)
+    cfg = TrainConfig(iterations=100)
+    n = len(gs)
+    for it in (1, 2, 3):
+        g = GradientSet.zeros(n)
+        for k in PARAM_CLASSES:
+            getattr(g, k)[...] = d[f"g{it}_{k}"]
+        adam_step(gs, g, opt, cfg, it)
+    for k in PARAM_CLASSES:
+        assert np.array_equal(getattr(gs, k), d["out_" + k]), k
+        assert np.array_equal(opt.m[k], d["m_" + k]) and np.array_equal(opt.v[k], d["v_" + k]), k
+
+
+def test_trainer_step_matches_reference_step():
+    from paper_2504_13339_b200 import scenes
+    from paper_2504_13339_b200.device import DeviceTF
+    from paper_2504_13339_b200.model import PARAM_CLASSES
+    from paper_2504_13339_b200.train import Trainer, TrainConfig, View
+
+    d = G.load("train_step")
+    learned = scenes.random_gaussians(2000, seed=0)
+    tf = scenes.random_tf(2, 4)
+    cams = scenes.orbit_cameras(2, 3, 64, 64)
+    tr = Trainer(learned, TrainConfig(iterations=100))
+    dtf = DeviceTF(tf)
+    views = [View(c, dtf, torch.from_numpy(d[f"target{i}"]).cuda()) for i, c in enumerate(cams)]
+    loss = float(tr.step(views, iteration=1).item())
+    assert abs(loss - float(np.mean(d["losses"]))) <= 1e-5 * abs(float(np.mean(d["losses"])))
+    out = tr.gaussians()
+    before = learned
+    for k in PARAM_CLASSES:
+        step_ref = d["out_" + k] - getattr(before, k)
+        step_gpu = getattr(out, k) - getattr(before, k)
+        # Adam's first step is +-lr wherever |g| >> eps: compare the update itself
+        assert G.norm_rel(step_gpu, step_ref) <= 1e-3, k
+
+
+# -- full-size properties (config 2 geometry, one view) ---------------------------------
+
+def test_c2_view_properties():
+    from paper_2504_13339_b200 import scenes
+    from paper_2504_13339_b200.device import DeviceTF, Rasterizer
+
+    gs, _, tf, cams = scenes.config_scene("c2")
+    rz = Rasterizer()
+    params = torch.from_numpy(gs.pack()).cuda()
+    fr = rz.forward(params, len(gs), DeviceTF(tf), cams[0], want_order=True)
+    n_inst = fr.n_inst
+    assert n_inst > 10_000_000
+    t = fr.out_t.cpu().numpy()
+    assert np.all((t >= 0) & (t <= 1))
+    last = fr.out_last.cpu().numpy()
+    assert last.max() < n_inst and last.min() >= -1
+    ncon = fr.n_contrib.cpu().numpy()
+    assert np.all(ncon >= 0) and np.all((ncon == 0) == (last == -1))
+    # sorted keys: tiles non-decreasing and ranges partition the instance list
+    ts, te = fr.tile_start.cpu().numpy(), fr.tile_end.cpu().numpy()
+    assert ts[0] == 0 and te[-1] == n_inst and np.all(ts[1:] == te[:-1]) and np.all(te >= ts)
+    # every pixel's last contributor lies inside its tile's range
+    h, w = fr.height, fr.width
+    tiles = (np.arange(h)[:, None] // 16) * ((w + 15) // 16) + (np.arange(w)[None, :] // 16)
+    has = last >= 0
+    assert np.all(last[has] >= ts[tiles[has]]) and np.all(last[has] < te[tiles[has]])
+    # the gradient buffer is finite and deterministic
+    d_img = torch.rand(h, w, 3, device="cuda") - 0.5
+    g1 = rz.backward(fr, d_img).clone()
+    g2 = rz.backward(fr, d_img)
+    assert torch.isfinite(g1).all() and torch.equal(g1, g2)
