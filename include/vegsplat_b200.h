@@ -154,13 +154,13 @@ int vegs_composite_backward(const int32_t *tile_start, const int32_t *tile_end,
 /* Per-Gaussian: float64 reduction of its instance rows (duplicate order == np.add.at
  * order), then projection and shading backward.  grads: flat float64 class-major
  * buffer (19 n); grads = accumulate ? grads + scale * g : scale * g.  viewspace_norm /
- * visible may be NULL. */
+ * visible may be NULL.  ws holds the per-Gaussian sums (n x (6 + C) float64). */
 int vegs_preprocess_backward(const double *params, int64_t n, const VegsCamera *cam,
                              const VegsTF *tf, const VegsSettings *st, int32_t n_channels,
                              int32_t store_f64, const uint32_t *tiles, const int64_t *offsets,
                              const void *inst_rows, double scale, int32_t accumulate,
                              double *grads, double *viewspace_norm, uint8_t *visible,
-                             void *stream);
+                             void *ws, size_t *ws_bytes, void *stream);
 
 /* ---- drop-in raw kernels (reference argument lists) -------------------------------- */
 int vegs_blend_forward(const int64_t *tile_start, const int64_t *tile_end, int64_t n_tiles,

@@ -319,12 +319,40 @@ __global__ void __launch_bounds__(256) table_from_arrays_kernel(
 }
 
 // ---------------------------------------------------------------------------------
-// Backward: reduce the instance rows of Gaussian g, then projection and shading adjoints.
+// Backward, part 1: float64 sum of each kept Gaussian's instance rows, in duplicate order
+// (== sorted-instance order per splat, the order np.add.at applies at pipeline.py:313-316).
+// A lean kernel (few registers, full occupancy, 16-byte loads) so the ~1 GB of rows per
+// 1024^2 view streams near bandwidth; the register-heavy chain runs separately.
 
-template <typename Real>
+template <typename Real, int NV>
+__global__ void __launch_bounds__(256) reduce_rows_kernel(const uint32_t *tiles, const int64_t *offsets,
+                                                          const Real *rows, int64_t n, double *sums) {
+    const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (g >= n) return;
+    const uint32_t cnt = tiles[g];
+    if (cnt == 0) return;
+    constexpr int RS = ((7 + (NV - 6)) + 3) & ~3;
+    constexpr int NF4 = (int)(RS * sizeof(Real) / 16);
+    double acc[NV];
+#pragma unroll
+    for (int k = 0; k < NV; ++k) acc[k] = 0.0;
+    const float4 *src = reinterpret_cast<const float4 *>(rows + (int64_t)RS * offsets[g]);
+    for (uint32_t i = 0; i < cnt; ++i, src += NF4) {
+        Real row[RS];
+#pragma unroll
+        for (int k = 0; k < NF4; ++k) reinterpret_cast<float4 *>(row)[k] = __ldg(src + k);
+#pragma unroll
+        for (int k = 0; k < NV; ++k) acc[k] = acc[k] + (double)row[k];
+    }
+#pragma unroll
+    for (int k = 0; k < NV; ++k) sums[(int64_t)NV * g + k] = acc[k];
+}
+
+// Backward, part 2: projection and shading adjoints per Gaussian (float64).
+
 __global__ void __launch_bounds__(256) preprocess_bwd_kernel(
     const double *params, int64_t n, VegsCamera cam, VegsTF tf, VegsSettings st, int n_ch,
-    const uint32_t *tiles, const int64_t *offsets, const Real *rows, double scale, int accumulate,
+    const uint32_t *tiles, const double *sums, double scale, int accumulate,
     double *grads, double *vs_norm, uint8_t *visible_out) {
     extern __shared__ double tf_smem[];
     const TFTable tab = stage_tf(tf, tf_smem);
@@ -344,14 +372,7 @@ __global__ void __launch_bounds__(256) preprocess_bwd_kernel(
         if (visible_out) visible_out[g] = 0;
         return;
     }
-    // float64 reduction in duplicate order == sorted order per splat (np.add.at)
-    const int rs = rec_stride(n_ch);
-    double red[6 + 11];
-    const int nred = row_width(n_ch);
-    for (int k = 0; k < nred; ++k) red[k] = 0.0;
-    const Real *row = rows + (int64_t)rs * offsets[g];
-    for (uint32_t i = 0; i < cnt; ++i, row += rs)
-        for (int k = 0; k < nred; ++k) red[k] = red[k] + (double)row[k];
+    const double *red = sums + (int64_t)row_width(n_ch) * g;  // reduce_rows_kernel output
     const double gmx = red[0], gmy = red[1];
     const double d_con[3] = {red[2], red[3], red[4]};
     const double d_ab = red[5];
@@ -611,28 +632,33 @@ extern "C" int vegs_preprocess_backward(const double *params, int64_t n, const V
                                         const VegsTF *tf, const VegsSettings *st, int32_t n_channels,
                                         int32_t store_f64, const uint32_t *tiles, const int64_t *offsets,
                                         const void *inst_rows, double scale, int32_t accumulate,
-                                        double *grads, double *viewspace_norm, uint8_t *visible,
-                                        void *stream) {
-    if (!cam || !st || !tf_ok(tf) || (n > 0 && (!params || !tiles || !offsets || !grads)))
+                                        double *grads, double *viewspace_norm, uint8_t *visible, void *ws,
+                                        size_t *ws_bytes, void *stream) {
+    if (!ws_bytes || (n_channels != 3 && n_channels != 11)) return VEGS_ERR_ARG;
+    const size_t need = sizeof(double) * (size_t)row_width(n_channels) * (size_t)(n > 0 ? n : 1);
+    if (!ws) {
+        *ws_bytes = need;
+        return VEGS_OK;
+    }
+    if (*ws_bytes < need) return VEGS_ERR_CAPACITY;
+    if (!cam || !st || !tf_ok(tf) || (n > 0 && (!params || !tiles || !offsets || !grads || !inst_rows)))
         return VEGS_ERR_ARG;
-    if (n_channels != 3 && n_channels != 11) return VEGS_ERR_ARG;
     if (n == 0) return VEGS_OK;
-    const size_t smem = tf_smem_bytes(*tf);
     const int blocks = (int)((n + 255) / 256);
     cudaStream_t s = (cudaStream_t)stream;
+    double *sums = (double *)ws;
     if (store_f64) {
-        VEGS_CUDA(cudaFuncSetAttribute(preprocess_bwd_kernel<double>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        preprocess_bwd_kernel<double><<<blocks, 256, smem, s>>>(
-            params, n, *cam, *tf, *st, n_channels, tiles, offsets, (const double *)inst_rows, scale,
-            accumulate, grads, viewspace_norm, visible);
+        if (n_channels == 3) reduce_rows_kernel<double, 9><<<blocks, 256, 0, s>>>(tiles, offsets, (const double *)inst_rows, n, sums);
+        else reduce_rows_kernel<double, 17><<<blocks, 256, 0, s>>>(tiles, offsets, (const double *)inst_rows, n, sums);
     } else {
-        VEGS_CUDA(cudaFuncSetAttribute(preprocess_bwd_kernel<float>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        preprocess_bwd_kernel<float><<<blocks, 256, smem, s>>>(
-            params, n, *cam, *tf, *st, n_channels, tiles, offsets, (const float *)inst_rows, scale,
-            accumulate, grads, viewspace_norm, visible);
+        if (n_channels == 3) reduce_rows_kernel<float, 9><<<blocks, 256, 0, s>>>(tiles, offsets, (const float *)inst_rows, n, sums);
+        else reduce_rows_kernel<float, 17><<<blocks, 256, 0, s>>>(tiles, offsets, (const float *)inst_rows, n, sums);
     }
+    VEGS_CHECK_LAUNCH();
+    const size_t smem = tf_smem_bytes(*tf);
+    VEGS_CUDA(cudaFuncSetAttribute(preprocess_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    preprocess_bwd_kernel<<<blocks, 256, smem, s>>>(params, n, *cam, *tf, *st, n_channels, tiles, sums, scale,
+                                                    accumulate, grads, viewspace_norm, visible);
     VEGS_CHECK_LAUNCH();
     return VEGS_OK;
 }

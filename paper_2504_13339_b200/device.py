@@ -41,7 +41,7 @@ LAUNCHES = {
                                   # CUB key sort (hist + scan + 4 onesweep), finalize
     "vegs_composite_forward": 1,
     "vegs_composite_backward": 1,
-    "vegs_preprocess_backward": 1,
+    "vegs_preprocess_backward": 2,  # row reduction + chain
     "vegs_loss_l1_ssim": 2,
     "vegs_adam_step": 1,
 }
@@ -301,9 +301,12 @@ class Rasterizer:
         rows = self.backward_rows(fr, d_img, d_alpha)
         if grads is None:
             grads = torch.empty(19 * fr.n, dtype=torch.float64, device=self.device)
-        self._run("vegs_preprocess_backward", _p(fr.params), fr.n, ctypes.byref(fr.cam), ctypes.byref(fr.tf.struct),
-             ctypes.byref(fr.settings), fr.n_ch, int(fr.store_f64), _p(fr.tiles), _p(fr.offsets), _p(rows),
-             float(scale), int(accumulate), _p(grads), _p(viewspace_norm), _p(visible), _stream())
+        args = (_p(fr.params), fr.n, ctypes.byref(fr.cam), ctypes.byref(fr.tf.struct), ctypes.byref(fr.settings),
+                fr.n_ch, int(fr.store_f64), _p(fr.tiles), _p(fr.offsets), _p(rows), float(scale), int(accumulate),
+                _p(grads), _p(viewspace_norm), _p(visible))
+        wsz = _lib.size_query("vegs_preprocess_backward", *args, tail=(_stream(),))
+        ws = self._alloc().get("ws_pbwd", wsz, torch.uint8)
+        self._run("vegs_preprocess_backward", *args, _p(ws), ctypes.byref(ctypes.c_size_t(wsz)), _stream())
         return grads
 
 

@@ -319,6 +319,7 @@ def test_c2_view_properties():
     assert ts[0] == 0 and te[-1] == n_inst and np.all(ts[1:] == te[:-1]) and np.all(te >= ts)
     # every pixel's last contributor lies inside its tile's range
     h, w = fr.height, fr.width
+    last = last.reshape(h, w)
     tiles = (np.arange(h)[:, None] // 16) * ((w + 15) // 16) + (np.arange(w)[None, :] // 16)
     has = last >= 0
     assert np.all(last[has] >= ts[tiles[has]]) and np.all(last[has] < te[tiles[has]])
