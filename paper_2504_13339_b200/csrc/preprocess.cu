@@ -125,6 +125,7 @@ __device__ void shade_one(const ParamView &P, int64_t g, const TFTable &tf, cons
     s.visible = s.alpha_base >= st.cull_alpha;
 }
 
+template <bool kRect = true>
 __device__ void project_one(const ParamView &P, int64_t g, double alpha_base, const VegsCamera &cam,
                             const VegsSettings &st, Projected &p) {
     const double *W = cam.rot;
@@ -200,6 +201,10 @@ __device__ void project_one(const ParamView &P, int64_t g, double alpha_base, co
     p.conic[0] = p.c * inv_det;
     p.conic[1] = -p.b * inv_det;
     p.conic[2] = p.a * inv_det;
+    if constexpr (!kRect) {  // the backward only needs the projection, not the rect
+        p.keep = front && (p.det > 0);
+        return;
+    }
     const double ratio = fmax(alpha_base, st.alpha_skip) / st.alpha_skip;
     const double rc = sqrt(fmax(p.lam, 0.0) * 2.0 * log(ratio)) + st.rect_margin_px;
     const double Wd = (double)cam.width, Hd = (double)cam.height;
@@ -379,10 +384,13 @@ __global__ void __launch_bounds__(256) preprocess_bwd_kernel(
     const double *d_ch = red + 6;
 
     const ParamView P(params, n);
-    Shaded s;
-    shade_one(P, g, tab, cam, st, s);
+#define VEGS_PUT(dst, val) (dst) = accumulate ? (dst) + scale * (val) : scale * (val)
+    // projection adjoint first, its outputs written out before the shading recompute so
+    // the two halves' working sets are never live together
+    double gpos[3];
+    {
     Projected p;
-    project_one(P, g, s.alpha_base, cam, st, p);
+    project_one<false>(P, g, 0.0, cam, st, p);
     const double *W = cam.rot;
     const double f = cam.focal;
 
@@ -417,7 +425,6 @@ __global__ void __launch_bounds__(256) preprocess_bwd_kernel(
                   gJ[1][2] * (-2.0 * f * p.tyc * iz2 * iz + f * iz2 * dyz) +
                   gmx * (-f * p.t[0] * iz2) + gmy * (f * p.t[1] * iz2);
     if (n_ch == 11) g_tz += d_ch[3];
-    double gpos[3];
     for (int k = 0; k < 3; ++k) gpos[k] = g_tx * W[k] + g_ty * W[3 + k] + g_tz * W[6 + k];
     double s2[3], glog[3], gR[3][3];
     for (int k = 0; k < 3; ++k) s2[k] = p.scale[k] * p.scale[k];
@@ -443,6 +450,12 @@ __global__ void __launch_bounds__(256) preprocess_bwd_kernel(
     const double qd = fmax(p.q_norm, 1e-30);
     double grot[4];
     for (int k = 0; k < 4; ++k) grot[k] = (gq[k] - gqp * p.q_hat[k]) / qd;
+    for (int k = 0; k < 3; ++k) VEGS_PUT(G.log_scale[3 * g + k], glog[k]);
+    for (int k = 0; k < 4; ++k) VEGS_PUT(G.rot[4 * g + k], grot[k]);
+    }
+
+    Shaded s;
+    shade_one(P, g, tab, cam, st, s);
 
     // ---- shade_backward (shading.py:97-176)
     const double sa = fabs(s.ndotl);
@@ -493,13 +506,10 @@ __global__ void __launch_bounds__(256) preprocess_bwd_kernel(
     const double raw_value = g_v * s.v * (1.0 - s.v);
     const double raw_weight = d_ab * s.op * s.w * (1.0 - s.w);
 
-#define VEGS_PUT(dst, val) (dst) = accumulate ? (dst) + scale * (val) : scale * (val)
     for (int k = 0; k < 3; ++k) {
         VEGS_PUT(G.pos[3 * g + k], gpos[k]);
-        VEGS_PUT(G.log_scale[3 * g + k], glog[k]);
         VEGS_PUT(G.normal[3 * g + k], gnormal[k]);
     }
-    for (int k = 0; k < 4; ++k) VEGS_PUT(G.rot[4 * g + k], grot[k]);
     VEGS_PUT(G.raw_value[g], raw_value);
     VEGS_PUT(G.raw_weight[g], raw_weight);
     VEGS_PUT(G.raw_ka[g], raw_ka);
