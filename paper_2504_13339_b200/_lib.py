@@ -8,7 +8,7 @@ CUDA device is present, every compute call raises.
 from __future__ import annotations
 
 import ctypes
-from ctypes import POINTER, c_double, c_int32, c_int64, c_size_t, c_uint8, c_void_p
+from ctypes import POINTER, c_double, c_int32, c_int64, c_size_t, c_uint8, c_uint64, c_void_p
 from pathlib import Path
 
 LIB_PATH = Path(__file__).resolve().parent / "lib" / "libvegsplat_b200.so"
@@ -54,9 +54,10 @@ _SIGS = {
     "vegs_composite_forward": [P, P, P, P, P, c_int32, c_int32, P, c_int32, c_int32, c_double, c_double,
                                P, P, P, P, P],
     "vegs_composite_backward": [P, P, P, P, P, P, c_int32, c_int32, P, c_int32, c_int32, c_double, P, P,
-                                P, P, P, P],
+                                P, P, P, c_uint64, P],
     "vegs_preprocess_backward": [P, c_int64, POINTER(VegsCamera), POINTER(VegsTF), POINTER(VegsSettings),
-                                 c_int32, c_int32, P, P, P, c_double, c_int32, P, P, P, P, POINTER(c_size_t), P],
+                                 c_int32, c_int32, P, P, P, c_double, c_int32, P, P, P, c_uint64, P,
+                                 POINTER(c_size_t), P],
     "vegs_blend_forward": [P, P, c_int64, c_int64, c_int64, P, P, P, P, P, P, c_int32, c_int32, P, c_int64,
                            c_int64, c_double, c_double, P, P, P, P, P],
     "vegs_blend_backward": [P, P, c_int64, c_int64, c_int64, P, P, P, P, P, P, c_int32, c_int32, P, c_int64,
@@ -66,6 +67,14 @@ _SIGS = {
 }
 
 _lib = None
+_stamp = 0
+
+
+def next_stamp() -> int:
+    """Fresh 64-bit tag for backward row buffers (see vegs_composite_backward)."""
+    global _stamp
+    _stamp += 1
+    return (_stamp * 0x9E3779B97F4A7C15 + 1) & 0xFFFFFFFFFFFFFFFF
 
 
 class VegsError(RuntimeError):

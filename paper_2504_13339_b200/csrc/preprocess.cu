@@ -331,13 +331,15 @@ __global__ void __launch_bounds__(256) table_from_arrays_kernel(
 
 template <typename Real, int NV>
 __global__ void __launch_bounds__(256) reduce_rows_kernel(const uint32_t *tiles, const int64_t *offsets,
-                                                          const Real *rows, int64_t n, double *sums) {
+                                                          const Real *rows, int64_t n, uint64_t stamp,
+                                                          double *sums) {
     const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (g >= n) return;
     const uint32_t cnt = tiles[g];
     if (cnt == 0) return;
     constexpr int RS = ((7 + (NV - 6)) + 3) & ~3;
     constexpr int NF4 = (int)(RS * sizeof(Real) / 16);
+    const uint32_t s_lo = (uint32_t)stamp, s_hi = (uint32_t)(stamp >> 32);
     double acc[NV];
 #pragma unroll
     for (int k = 0; k < NV; ++k) acc[k] = 0.0;
@@ -346,6 +348,8 @@ __global__ void __launch_bounds__(256) reduce_rows_kernel(const uint32_t *tiles,
         Real row[RS];
 #pragma unroll
         for (int k = 0; k < NF4; ++k) reinterpret_cast<float4 *>(row)[k] = __ldg(src + k);
+        const uint32_t *tag = reinterpret_cast<const uint32_t *>(&row[NV]);
+        if (tag[0] != s_lo || tag[1] != s_hi) continue;  // instance not visited: contributes 0
 #pragma unroll
         for (int k = 0; k < NV; ++k) acc[k] = acc[k] + (double)row[k];
     }
@@ -642,8 +646,8 @@ extern "C" int vegs_preprocess_backward(const double *params, int64_t n, const V
                                         const VegsTF *tf, const VegsSettings *st, int32_t n_channels,
                                         int32_t store_f64, const uint32_t *tiles, const int64_t *offsets,
                                         const void *inst_rows, double scale, int32_t accumulate,
-                                        double *grads, double *viewspace_norm, uint8_t *visible, void *ws,
-                                        size_t *ws_bytes, void *stream) {
+                                        double *grads, double *viewspace_norm, uint8_t *visible,
+                                        uint64_t row_stamp, void *ws, size_t *ws_bytes, void *stream) {
     if (!ws_bytes || (n_channels != 3 && n_channels != 11)) return VEGS_ERR_ARG;
     const size_t need = sizeof(double) * (size_t)row_width(n_channels) * (size_t)(n > 0 ? n : 1);
     if (!ws) {
@@ -658,11 +662,11 @@ extern "C" int vegs_preprocess_backward(const double *params, int64_t n, const V
     cudaStream_t s = (cudaStream_t)stream;
     double *sums = (double *)ws;
     if (store_f64) {
-        if (n_channels == 3) reduce_rows_kernel<double, 9><<<blocks, 256, 0, s>>>(tiles, offsets, (const double *)inst_rows, n, sums);
-        else reduce_rows_kernel<double, 17><<<blocks, 256, 0, s>>>(tiles, offsets, (const double *)inst_rows, n, sums);
+        if (n_channels == 3) reduce_rows_kernel<double, 9><<<blocks, 256, 0, s>>>(tiles, offsets, (const double *)inst_rows, n, row_stamp, sums);
+        else reduce_rows_kernel<double, 17><<<blocks, 256, 0, s>>>(tiles, offsets, (const double *)inst_rows, n, row_stamp, sums);
     } else {
-        if (n_channels == 3) reduce_rows_kernel<float, 9><<<blocks, 256, 0, s>>>(tiles, offsets, (const float *)inst_rows, n, sums);
-        else reduce_rows_kernel<float, 17><<<blocks, 256, 0, s>>>(tiles, offsets, (const float *)inst_rows, n, sums);
+        if (n_channels == 3) reduce_rows_kernel<float, 9><<<blocks, 256, 0, s>>>(tiles, offsets, (const float *)inst_rows, n, row_stamp, sums);
+        else reduce_rows_kernel<float, 17><<<blocks, 256, 0, s>>>(tiles, offsets, (const float *)inst_rows, n, row_stamp, sums);
     }
     VEGS_CHECK_LAUNCH();
     const size_t smem = tf_smem_bytes(*tf);
