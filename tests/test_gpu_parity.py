@@ -328,3 +328,41 @@ def test_c2_view_properties():
     g1 = rz.backward(fr, d_img).clone()
     g2 = rz.backward(fr, d_img)
     assert torch.isfinite(g1).all() and torch.equal(g1, g2)
+
+
+# -- the benchmark's own scale: one config-2 view (1M Gaussians, 1024 x 1024) vs the oracle --
+
+@pytest.fixture(scope="module")
+def c2_case():
+    from paper_2504_13339_b200 import scenes
+
+    gs, _, tf, cams = scenes.config_scene("c2")
+    cam = cams[0]
+    img_o, st_o = O.render_with_state(gs, tf, cam, (1.0, 1.0, 1.0), S, False, np.float32)
+    img_g, st_g = R.render_with_state(gs, tf, cam, (1.0, 1.0, 1.0), S, False, np.float32)
+    return gs, tf, cam, img_o, st_o, img_g, st_g
+
+
+@pytest.mark.slow
+def test_c2_forward_bit_exact_vs_oracle(c2_case):
+    gs, tf, cam, img_o, st_o, img_g, st_g = c2_case
+    b = st_g.blend
+    assert len(b.order) > 10_000_000
+    assert np.array_equal(st_g.kept, st_o["kept"])
+    assert np.array_equal(st_g.proj.rect, st_o["proj"]["rect"])
+    assert np.array_equal(b.order, st_o["order"])
+    assert np.array_equal(b.tile_start, st_o["tile_start"]) and np.array_equal(b.tile_end, st_o["tile_end"])
+    assert np.array_equal(b.out_last, st_o["out_last"])
+    assert np.array_equal(b.n_contrib, st_o["n_contrib"])
+    assert np.array_equal(b.out_t, st_o["out_t"])
+    assert img_close(img_g.rgb, img_o["rgb"])
+
+
+@pytest.mark.slow
+def test_c2_backward_vs_oracle(c2_case):
+    gs, tf, cam, img_o, st_o, img_g, st_g = c2_case
+    d_rgb = np.random.default_rng(6).uniform(-1, 1, size=(cam.height, cam.width, 3))
+    g_o = O.rasterize_backward(st_o, d_rgb)
+    g_g = R.rasterize_backward(st_g, R.ImageGradients(rgb=d_rgb))
+    for k in O.GRAD_CLASSES:
+        assert G.norm_rel(getattr(g_g, k), g_o[k]) <= GRAD_REL_F32, (k, G.norm_rel(getattr(g_g, k), g_o[k]))
