@@ -23,6 +23,8 @@
  *   vegs_loss_l1_ssim           loss.py:80-168 ssim / ssim_backward / compute_loss (regularisers off)
  *   vegs_adam_step              train.py:176-195 adam_step (+ learning_rates :156-173 on the host)
  *   vegs_tf_eval                transfer.py:91-127 eval_opacity / eval_color / d_*_dv
+ *   vegs_densify_count / _apply train.py:237-284 densify_and_prune (+ DensifyStats.add :210-214,
+ *                               fused into vegs_preprocess_backward)
  */
 #ifndef VEGSPLAT_B200_H
 #define VEGSPLAT_B200_H
@@ -157,14 +159,16 @@ int vegs_composite_backward(const int32_t *tile_start, const int32_t *tile_end,
 /* Per-Gaussian: float64 reduction of its instance rows (duplicate order == np.add.at
  * order), then projection and shading backward.  grads: flat float64 class-major
  * buffer (19 n); grads = accumulate ? grads + scale * g : scale * g.  viewspace_norm /
- * visible may be NULL.  Only rows carrying row_stamp are summed.  ws holds the per-Gaussian
+ * visible may be NULL.  Only rows carrying row_stamp are summed.  densify_stats (n x 5,
+ * may be NULL) accumulates DensifyStats for the kept splats.  ws holds the per-Gaussian
  * sums (n x (6 + C) float64). */
 int vegs_preprocess_backward(const double *params, int64_t n, const VegsCamera *cam,
                              const VegsTF *tf, const VegsSettings *st, int32_t n_channels,
                              int32_t store_f64, const uint32_t *tiles, const int64_t *offsets,
                              const void *inst_rows, double scale, int32_t accumulate,
                              double *grads, double *viewspace_norm, uint8_t *visible,
-                             uint64_t row_stamp, void *ws, size_t *ws_bytes, void *stream);
+                             double *densify_stats, uint64_t row_stamp, void *ws, size_t *ws_bytes,
+                             void *stream);
 
 /* ---- drop-in raw kernels (reference argument lists) -------------------------------- */
 int vegs_blend_forward(const int64_t *tile_start, const int64_t *tile_end, int64_t n_tiles,
@@ -183,6 +187,30 @@ int vegs_blend_backward(const int64_t *tile_start, const int64_t *tile_end, int6
                         double alpha_clamp, const void *out_t, const int64_t *out_last,
                         const void *d_img, const void *d_alpha_plane, void *g_mean2d,
                         void *g_conic, void *g_alpha, void *g_channels, void *stream);
+
+/* ---- densify / prune (train.py:237-284) ------------------------------------------- */
+typedef struct {
+    double grad_threshold;   /* densify_grad_threshold */
+    double percent_dense;
+    double scene_extent;
+    double prune_threshold;  /* prune_weight_threshold on sigmoid(raw_weight) */
+    double position_lr;      /* clone step */
+    double log_split_factor; /* log(1.6) */
+    int32_t no_weights;      /* 1: pruning off */
+    int32_t pad_;
+} VegsDensify;
+
+/* stats: n x 5 float64 [sum viewspace_norm, sum position grad (3), count] (DensifyStats).
+ * flags / offsets: (n+1) x int4 = (keep, clone, split, split-any); offsets[n] holds the
+ * block totals.  Output rows n_out = tot.x + tot.y + 2 tot.z. */
+int vegs_densify_count(const double *params, int64_t n, const double *stats, const VegsDensify *dp,
+                       int32_t *flags, int32_t *offsets, void *ws, size_t *ws_bytes, void *stream);
+
+/* eps: 2 x tot.w x 3 float64 standard normals (round-major, as the reference draws them). */
+int vegs_densify_apply(const double *params, const double *m, const double *v, int64_t n,
+                       const double *stats, const VegsDensify *dp, const int32_t *flags,
+                       const int32_t *offsets, const double *eps, int64_t n_out, double *out_params,
+                       double *out_m, double *out_v, void *stream);
 
 /* ---- loss / optimiser ------------------------------------------------------------- */
 /* (w_l1) * mean|x - y| + lam * (1 - mean SSIM) on H x W x 3 float32 images; writes

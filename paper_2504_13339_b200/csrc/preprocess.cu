@@ -14,6 +14,8 @@
 
 #include <math.h>
 
+#include <cub/cub.cuh>
+
 #include "vegs_common.cuh"
 
 namespace vegs {
@@ -362,7 +364,7 @@ __global__ void __launch_bounds__(256) reduce_rows_kernel(const uint32_t *tiles,
 __global__ void __launch_bounds__(256) preprocess_bwd_kernel(
     const double *params, int64_t n, VegsCamera cam, VegsTF tf, VegsSettings st, int n_ch,
     const uint32_t *tiles, const double *sums, double scale, int accumulate,
-    double *grads, double *vs_norm, uint8_t *visible_out) {
+    double *grads, double *vs_norm, uint8_t *visible_out, double *dstats) {
     extern __shared__ double tf_smem[];
     const TFTable tab = stage_tf(tf, tf_smem);
     const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -521,9 +523,14 @@ __global__ void __launch_bounds__(256) preprocess_bwd_kernel(
     VEGS_PUT(G.raw_ks[g], raw_ks);
     VEGS_PUT(G.raw_beta[g], raw_beta);
 #undef VEGS_PUT
-    if (vs_norm) {
-        const double ax = gmx * (0.5 * cam.width), ay = gmy * (0.5 * cam.height);
-        vs_norm[g] = sqrt(ax * ax + ay * ay);
+    const double ax = gmx * (0.5 * cam.width), ay = gmy * (0.5 * cam.height);
+    const double vsn = sqrt(ax * ax + ay * ay);  // pipeline.py:355-358 (half-resolution NDC units)
+    if (vs_norm) vs_norm[g] = vsn;
+    if (dstats) {  // DensifyStats.add (train.py:210-214) for this view
+        double *st5 = dstats + 5 * g;
+        st5[0] = st5[0] + vsn;
+        for (int k = 0; k < 3; ++k) st5[1 + k] = st5[1 + k] + gpos[k];
+        st5[4] = st5[4] + 1.0;
     }
     if (visible_out) visible_out[g] = 1;
 }
@@ -647,7 +654,8 @@ extern "C" int vegs_preprocess_backward(const double *params, int64_t n, const V
                                         int32_t store_f64, const uint32_t *tiles, const int64_t *offsets,
                                         const void *inst_rows, double scale, int32_t accumulate,
                                         double *grads, double *viewspace_norm, uint8_t *visible,
-                                        uint64_t row_stamp, void *ws, size_t *ws_bytes, void *stream) {
+                                        double *densify_stats, uint64_t row_stamp, void *ws, size_t *ws_bytes,
+                                        void *stream) {
     if (!ws_bytes || (n_channels != 3 && n_channels != 11)) return VEGS_ERR_ARG;
     const size_t need = sizeof(double) * (size_t)row_width(n_channels) * (size_t)(n > 0 ? n : 1);
     if (!ws) {
@@ -672,7 +680,7 @@ extern "C" int vegs_preprocess_backward(const double *params, int64_t n, const V
     const size_t smem = tf_smem_bytes(*tf);
     VEGS_CUDA(cudaFuncSetAttribute(preprocess_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     preprocess_bwd_kernel<<<blocks, 256, smem, s>>>(params, n, *cam, *tf, *st, n_channels, tiles, sums, scale,
-                                                    accumulate, grads, viewspace_norm, visible);
+                                                    accumulate, grads, viewspace_norm, visible, densify_stats);
     VEGS_CHECK_LAUNCH();
     return VEGS_OK;
 }
@@ -690,6 +698,173 @@ extern "C" int vegs_adam_step(double *params, const double *grads, double *m, do
     if (blocks > sms * 16) blocks = sms * 16;
     adam_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>(params, grads, m, v, n, lr, grad_scale, bias1,
                                                           bias2, nonfinite);
+    VEGS_CHECK_LAUNCH();
+    return VEGS_OK;
+}
+
+// ---------------------------------------------------------------------------------
+// Densify / prune (train.py:237-284), float64, reproducing the reference's output order:
+//   [kept originals that survive | surviving clones | surviving split children, round 0 |
+//    round 1], each block in Gaussian order, optimizer moments kept for originals and zero
+//   for new rows.  Split offsets use host-drawn normals eps[round][split_rank][3] so the
+//   caller can replay the reference's rng.standard_normal draws exactly.
+
+namespace vegs {
+
+struct Int4Sum {
+    __device__ __forceinline__ int4 operator()(const int4 &a, const int4 &b) const {
+        return make_int4(a.x + b.x, a.y + b.y, a.z + b.z, a.w + b.w);
+    }
+};
+
+__device__ __forceinline__ void densify_flags(const ParamView &P, int64_t g, const double *stats,
+                                              const VegsDensify &dp, bool &small, bool &big, bool &survive) {
+    const double cnt = fmax(stats[5 * g + 4], 1.0);
+    const bool cand = stats[5 * g] / cnt > dp.grad_threshold;
+    double ms = exp(P.log_scale[3 * g]);
+    ms = fmax(ms, exp(P.log_scale[3 * g + 1]));
+    ms = fmax(ms, exp(P.log_scale[3 * g + 2]));
+    small = cand && ms <= dp.percent_dense * dp.scene_extent;
+    big = cand && !small;
+    survive = dp.no_weights || sigmoid(P.raw_weight[g]) >= dp.prune_threshold;
+}
+
+__global__ void densify_classify_kernel(const double *params, int64_t n, const double *stats, VegsDensify dp,
+                                        int4 *flags) {
+    const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (g > n) return;
+    if (g == n) {
+        flags[g] = make_int4(0, 0, 0, 0);
+        return;
+    }
+    const ParamView P(params, n);
+    bool small, big, surv;
+    densify_flags(P, g, stats, dp, small, big, surv);
+    flags[g] = make_int4(!big && surv, small && surv, big && surv, big);
+}
+
+__device__ __forceinline__ void copy_row(const double *src, int64_t n, int64_t g, double *dst, int64_t n_out,
+                                         int64_t r) {
+    ParamView S(src, n);
+    GradView D(dst, n_out);
+    for (int k = 0; k < 3; ++k) {
+        D.pos[3 * r + k] = S.pos[3 * g + k];
+        D.log_scale[3 * r + k] = S.log_scale[3 * g + k];
+        D.normal[3 * r + k] = S.normal[3 * g + k];
+    }
+    for (int k = 0; k < 4; ++k) D.rot[4 * r + k] = S.rot[4 * g + k];
+    D.raw_value[r] = S.raw_value[g];
+    D.raw_weight[r] = S.raw_weight[g];
+    D.raw_ka[r] = S.raw_ka[g];
+    D.raw_kd[r] = S.raw_kd[g];
+    D.raw_ks[r] = S.raw_ks[g];
+    D.raw_beta[r] = S.raw_beta[g];
+}
+
+__device__ __forceinline__ void zero_row(double *dst, int64_t n_out, int64_t r) {
+    GradView D(dst, n_out);
+    for (int k = 0; k < 3; ++k) D.pos[3 * r + k] = D.log_scale[3 * r + k] = D.normal[3 * r + k] = 0.0;
+    for (int k = 0; k < 4; ++k) D.rot[4 * r + k] = 0.0;
+    D.raw_value[r] = D.raw_weight[r] = D.raw_ka[r] = D.raw_kd[r] = D.raw_ks[r] = D.raw_beta[r] = 0.0;
+}
+
+__global__ void densify_apply_kernel(const double *params, const double *m, const double *v, int64_t n,
+                                     const double *stats, VegsDensify dp, const int4 *flags, const int4 *offs,
+                                     const double *eps, int64_t n_out, double *out_params, double *out_m,
+                                     double *out_v) {
+    const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (g >= n) return;
+    const int4 f = flags[g];
+    if (!(f.x | f.y | f.z)) return;
+    const int4 o = offs[g], tot = offs[n];
+    const ParamView P(params, n);
+    if (f.x) {
+        copy_row(params, n, g, out_params, n_out, o.x);
+        copy_row(m, n, g, out_m, n_out, o.x);
+        copy_row(v, n, g, out_v, n_out, o.x);
+    }
+    if (f.y) {  // clone: step along the negative mean positional gradient (train.py:255-259)
+        const int64_t r = (int64_t)tot.x + o.y;
+        copy_row(params, n, g, out_params, n_out, r);
+        zero_row(out_m, n_out, r);
+        zero_row(out_v, n_out, r);
+        const double cnt = fmax(stats[5 * g + 4], 1.0);
+        double d[3], nn = 0.0;
+        for (int k = 0; k < 3; ++k) {
+            d[k] = stats[5 * g + 1 + k] / cnt;
+            nn = nn + d[k] * d[k];
+        }
+        const double norm = sqrt(nn);
+        GradView D(out_params, n_out);
+        for (int k = 0; k < 3; ++k) {
+            const double dir = norm > 0 ? d[k] / fmax(norm, 1e-30) : 0.0;
+            D.pos[3 * r + k] = P.pos[3 * g + k] - dp.position_lr * dir;
+        }
+    }
+    if (f.z) {  // split into two children (train.py:261-271)
+        double q[4], qq = 0.0;
+        for (int k = 0; k < 4; ++k) {
+            q[k] = P.rot[4 * g + k];
+            qq = qq + q[k] * q[k];
+        }
+        const double qn = sqrt(qq);
+        for (int k = 0; k < 4; ++k) q[k] = q[k] / qn;
+        const double w = q[0], x = q[1], y = q[2], z = q[3];
+        const double R[3][3] = {{1 - 2 * (y * y + z * z), 2 * (x * y - w * z), 2 * (x * z + w * y)},
+                                {2 * (x * y + w * z), 1 - 2 * (x * x + z * z), 2 * (y * z - w * x)},
+                                {2 * (x * z - w * y), 2 * (y * z + w * x), 1 - 2 * (x * x + y * y)}};
+        double sc[3];
+        for (int k = 0; k < 3; ++k) sc[k] = exp(P.log_scale[3 * g + k]);
+        for (int round = 0; round < 2; ++round) {
+            const int64_t r = (int64_t)tot.x + tot.y + (int64_t)round * tot.z + o.z;
+            copy_row(params, n, g, out_params, n_out, r);
+            zero_row(out_m, n_out, r);
+            zero_row(out_v, n_out, r);
+            const double *e = eps + ((int64_t)round * tot.w + o.w) * 3;
+            GradView D(out_params, n_out);
+            for (int i = 0; i < 3; ++i) {
+                double off = 0.0;
+                for (int j = 0; j < 3; ++j) off = off + R[i][j] * (sc[j] * e[j]);
+                D.pos[3 * r + i] = P.pos[3 * g + i] + off;
+                D.log_scale[3 * r + i] = P.log_scale[3 * g + i] - dp.log_split_factor;
+            }
+        }
+    }
+}
+
+}  // namespace vegs
+
+extern "C" int vegs_densify_count(const double *params, int64_t n, const double *stats, const VegsDensify *dp,
+                                  int32_t *flags, int32_t *offsets, void *ws, size_t *ws_bytes, void *stream) {
+    if (!ws_bytes || !dp) return VEGS_ERR_ARG;
+    size_t scan_bytes = 0;
+    int4 *dummy = nullptr;
+    VEGS_CUDA(cub::DeviceScan::ExclusiveScan(nullptr, scan_bytes, dummy, dummy, Int4Sum(), make_int4(0, 0, 0, 0),
+                                             n + 1, (cudaStream_t)stream));
+    if (!ws) {
+        *ws_bytes = scan_bytes;
+        return VEGS_OK;
+    }
+    if (*ws_bytes < scan_bytes) return VEGS_ERR_CAPACITY;
+    if (n >= (int64_t(1) << 30) || !flags || !offsets || (n > 0 && (!params || !stats))) return VEGS_ERR_ARG;
+    cudaStream_t s = (cudaStream_t)stream;
+    densify_classify_kernel<<<(int)((n + 1 + 255) / 256), 256, 0, s>>>(params, n, stats, *dp, (int4 *)flags);
+    VEGS_CHECK_LAUNCH();
+    VEGS_CUDA(cub::DeviceScan::ExclusiveScan(ws, scan_bytes, (int4 *)flags, (int4 *)offsets, Int4Sum(),
+                                             make_int4(0, 0, 0, 0), n + 1, s));
+    return VEGS_OK;
+}
+
+extern "C" int vegs_densify_apply(const double *params, const double *m, const double *v, int64_t n,
+                                  const double *stats, const VegsDensify *dp, const int32_t *flags,
+                                  const int32_t *offsets, const double *eps, int64_t n_out, double *out_params,
+                                  double *out_m, double *out_v, void *stream) {
+    if (!dp || (n > 0 && (!params || !m || !v || !stats || !flags || !offsets)) ||
+        (n_out > 0 && (!out_params || !out_m || !out_v)))
+        return VEGS_ERR_ARG;
+    if (n == 0) return VEGS_OK;
+    densify_apply_kernel<<<(int)((n + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
+        params, m, v, n, stats, *dp, (const int4 *)flags, (const int4 *)offsets, eps, n_out, out_params, out_m, out_v);
     VEGS_CHECK_LAUNCH();
     return VEGS_OK;
 }

@@ -44,6 +44,8 @@ LAUNCHES = {
     "vegs_preprocess_backward": 2,  # row reduction + chain
     "vegs_loss_l1_ssim": 2,
     "vegs_adam_step": 1,
+    "vegs_densify_count": 3,
+    "vegs_densify_apply": 1,
 }
 
 
@@ -296,7 +298,8 @@ class Rasterizer:
 
     def backward(self, fr: Frame, d_img: torch.Tensor, d_alpha: torch.Tensor | None = None,
                  grads: torch.Tensor | None = None, scale: float = 1.0, accumulate: bool = False,
-                 viewspace_norm: torch.Tensor | None = None, visible: torch.Tensor | None = None) -> torch.Tensor:
+                 viewspace_norm: torch.Tensor | None = None, visible: torch.Tensor | None = None,
+                 densify_stats: torch.Tensor | None = None) -> torch.Tensor:
         """Full analytic backward into the flat float64 gradient buffer (19 n)."""
         if fr.params is None:
             raise ValueError("backward through the full chain needs a Frame from forward()")
@@ -305,7 +308,7 @@ class Rasterizer:
             grads = torch.empty(19 * fr.n, dtype=torch.float64, device=self.device)
         args = (_p(fr.params), fr.n, ctypes.byref(fr.cam), ctypes.byref(fr.tf.struct), ctypes.byref(fr.settings),
                 fr.n_ch, int(fr.store_f64), _p(fr.tiles), _p(fr.offsets), _p(rows), float(scale), int(accumulate),
-                _p(grads), _p(viewspace_norm), _p(visible), ctypes.c_uint64(fr.row_stamp))
+                _p(grads), _p(viewspace_norm), _p(visible), _p(densify_stats), ctypes.c_uint64(fr.row_stamp))
         wsz = _lib.size_query("vegs_preprocess_backward", *args, tail=(_stream(),))
         ws = self._alloc().get("ws_pbwd", wsz, torch.uint8)
         self._run("vegs_preprocess_backward", *args, _p(ws), ctypes.byref(ctypes.c_size_t(wsz)), _stream())

@@ -185,6 +185,7 @@ class Trainer:
         self.step_count = 0
         self.rz = Rasterizer(settings, 3, store_f64=False, pooled=True)
         self.group = group
+        self.densify_stats = None  # (n, 5) float64 when densification is tracked
         self._d_img = None
         self._sums = None
 
@@ -198,7 +199,8 @@ class Trainer:
         if self._d_img is None or self._d_img.numel() != img.numel():
             self._d_img = torch.empty_like(img)
         l1_ssim_device(img, view.target, self.w_l1, self.lam, self._d_img, sums)
-        self.rz.backward(fr, self._d_img, None, self.grads, scale=scale, accumulate=not first)
+        self.rz.backward(fr, self._d_img, None, self.grads, scale=scale, accumulate=not first,
+                         densify_stats=self.densify_stats)
 
     def step(self, views: list[View], total_views: int | None = None, iteration: int | None = None,
              scene_extent: float = 1.0) -> torch.Tensor:
@@ -224,7 +226,113 @@ class Trainer:
         per_view = self.w_l1 * sums[:, 0] / n_el + self.lam * (1.0 - sums[:, 1] / n_pos)
         return per_view.mean()
 
+    def track_densify(self, on: bool = True) -> None:
+        """Accumulate DensifyStats (per view, fused into the backward) from now on."""
+        self.densify_stats = torch.zeros(self.n * 5, dtype=torch.float64, device=self.device) if on else None
+
+    def densify_and_prune(self, scene_extent: float, rng: np.random.Generator, position_lr: float) -> int:
+        """Device densify/prune of the resident set; the step's buffers are resized and
+        the densification statistics reset.  With world_size > 1 the statistics are
+        all-reduced first so every replica makes the same decision.  Returns the new n."""
+        if self.densify_stats is None:
+            raise RuntimeError("call track_densify() before training steps to collect statistics")
+        allreduce_gradients(self.densify_stats, self.group)
+        p, m, v, n_out = densify_device(self.params, self.m, self.v, self.n, self.densify_stats, self.config,
+                                        scene_extent, rng, position_lr)
+        self.params, self.m, self.v, self.n = p.clone(), m.clone(), v.clone(), n_out
+        self.grads = torch.zeros_like(self.params)
+        self.densify_stats = torch.zeros(self.n * 5, dtype=torch.float64, device=self.device)
+        return n_out
+
+    def reset_weights(self) -> None:
+        from .model import class_offsets, logit
+
+        a, b, _ = class_offsets(self.n)["raw_weight"]
+        self.params[a:b].clamp_(max=float(logit(WEIGHT_RESET_VALUE)))
+        self.m[a:b].zero_()
+        self.v[a:b].zero_()
+
     def check_finite(self) -> None:
         bad = self.nonfinite.cpu().numpy()
         if bad.any():
             raise TrainingError(f"non-finite gradient in parameter class {PARAM_CLASSES[int(np.argmax(bad))]!r}")
+
+
+# -- densification (train.py:200-284) on the device --------------------------------------
+
+SPLIT_SCALE_FACTOR = 1.6
+WEIGHT_RESET_VALUE = 0.01
+
+
+def _densify_struct(config: TrainConfig, scene_extent: float, position_lr: float):
+    from ._lib import VegsDensify
+
+    return VegsDensify(config.densify_grad_threshold, config.percent_dense, float(scene_extent),
+                       config.prune_weight_threshold, float(position_lr), math.log(SPLIT_SCALE_FACTOR),
+                       int(config.no_weights), 0)
+
+
+def densify_device(params: torch.Tensor, m: torch.Tensor, v: torch.Tensor, n: int, stats: torch.Tensor,
+                   config: TrainConfig, scene_extent: float, rng: np.random.Generator, position_lr: float):
+    """Clone / split / prune on device buffers; returns (params, m, v, n_out).
+
+    The split offsets are drawn on the host from ``rng`` exactly as the reference does
+    (two rounds of ``standard_normal((n_split, 3))``), so a seeded run reproduces it."""
+    import ctypes
+
+    from . import _lib
+    from .device import _p, _stream
+
+    dev = params.device
+    dp = _densify_struct(config, scene_extent, position_lr)
+    flags = torch.empty(4 * (n + 1), dtype=torch.int32, device=dev)
+    offs = torch.empty_like(flags)
+    nbytes = _lib.size_query("vegs_densify_count", _p(params), n, _p(stats), ctypes.byref(dp), _p(flags), _p(offs),
+                             tail=(_stream(),))
+    ws = torch.empty(max(nbytes, 1), dtype=torch.uint8, device=dev)
+    _lib.call("vegs_densify_count", _p(params), n, _p(stats), ctypes.byref(dp), _p(flags), _p(offs), _p(ws),
+              ctypes.byref(ctypes.c_size_t(nbytes)), _stream())
+    keep, clone, split, n_split = (int(x) for x in offs[4 * n:4 * n + 4].tolist())
+    if n_split:
+        eps_h = np.concatenate([rng.standard_normal(size=(n_split, 3)) for _ in range(2)])
+    else:
+        eps_h = np.zeros((0, 3))
+    eps = torch.from_numpy(np.ascontiguousarray(eps_h, dtype=np.float64)).to(dev)
+    n_out = keep + clone + 2 * split
+    out = [torch.empty(19 * max(n_out, 1), dtype=torch.float64, device=dev) for _ in range(3)]
+    _lib.call("vegs_densify_apply", _p(params), _p(m), _p(v), n, _p(stats), ctypes.byref(dp), _p(flags), _p(offs),
+              _p(eps), n_out, _p(out[0]), _p(out[1]), _p(out[2]), _stream())
+    return out[0][:19 * n_out], out[1][:19 * n_out], out[2][:19 * n_out], n_out
+
+
+def densify_and_prune(gs: GaussianSet, opt: OptimizerState, stats: DensifyStats, config: TrainConfig,
+                      scene_extent: float, rng: np.random.Generator, position_lr: float) -> GaussianSet:
+    """Reference-signature densify/prune (train.py:237-284): numpy in/out, GPU compute."""
+    dev = require_cuda()
+    n = len(gs)
+
+    def flat(d):
+        return torch.from_numpy(np.concatenate([np.asarray(d[k], dtype=np.float64).ravel()
+                                                for k in PARAM_CLASSES])).to(dev)
+
+    st = torch.from_numpy(np.ascontiguousarray(np.concatenate(
+        [stats.grad_accum[:, None], stats.pos_accum, stats.count[:, None]], axis=1), dtype=np.float64)).to(dev)
+    p, m, v, n_out = densify_device(torch.from_numpy(gs.pack()).to(dev), flat(opt.m), flat(opt.v), n, st, config,
+                                    scene_extent, rng, position_lr)
+    out = GaussianSet.unpack(p.cpu().numpy(), n_out)
+    mm = GaussianSet.unpack(m.cpu().numpy(), n_out)
+    vv = GaussianSet.unpack(v.cpu().numpy(), n_out)
+    opt.m = {k: getattr(mm, k) for k in PARAM_CLASSES}
+    opt.v = {k: getattr(vv, k) for k in PARAM_CLASSES}
+    stats.grad_accum, stats.pos_accum, stats.count = np.zeros(n_out), np.zeros((n_out, 3)), np.zeros(n_out)
+    return out
+
+
+def reset_weights(gs: GaussianSet, opt: OptimizerState) -> None:
+    """Cap activated weights and clear their moments (train.py:227-234)."""
+    from .model import logit
+
+    cap = float(logit(WEIGHT_RESET_VALUE))
+    np.minimum(gs.raw_weight, cap, out=gs.raw_weight)
+    opt.m["raw_weight"][:] = 0.0
+    opt.v["raw_weight"][:] = 0.0

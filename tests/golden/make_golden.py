@@ -284,6 +284,31 @@ def main():
     ts["losses"] = np.array(losses)
     save("train_step", ts)
 
+    # -- densify / prune (train.py:237-284): clones, splits (seeded rng) and weight pruning
+    rng_d = np.random.default_rng(42)
+    gd = scenes.random_gaussians(600, seed=41)
+    gd.raw_weight[:] = rng_d.normal(-2.0, 2.5, size=600)
+    gd.log_scale[:] += rng_d.uniform(-1.0, 2.0, size=(600, 1))
+    rgd = to_ref_gs(vs, gd)
+    opt = vtrain.OptimizerState.for_set(rgd)
+    for d_ in (opt.m, opt.v):
+        for k in d_:
+            d_[k][...] = rng_d.normal(size=d_[k].shape)
+    stats = vtrain.DensifyStats.zeros(600)
+    stats.grad_accum[:] = rng_d.uniform(0.0, 1e-3, size=600)
+    stats.pos_accum[:] = rng_d.normal(size=(600, 3))
+    stats.count[:] = rng_d.integers(0, 5, size=600)
+    dd = {"in_" + k: np.array(v) for k, v in rgd.arrays().items()}
+    dd.update({"in_m_" + k: v.copy() for k, v in opt.m.items()})
+    dd.update({"in_v_" + k: v.copy() for k, v in opt.v.items()})
+    dd.update(stats_grad=stats.grad_accum.copy(), stats_pos=stats.pos_accum.copy(), stats_count=stats.count.copy())
+    cfg_d = vtrain.TrainConfig(iterations=100)
+    out = vtrain.densify_and_prune(rgd, opt, stats, cfg_d, 3.0, np.random.default_rng(7), 1e-3)
+    dd.update({"out_" + k: np.array(v) for k, v in out.arrays().items()})
+    dd.update({"out_m_" + k: v for k, v in opt.m.items()})
+    dd.update({"out_v_" + k: v for k, v in opt.v.items()})
+    save("densify", dd)
+
     for k, v in saved.items():
         print(f"{k:20s} {v / 1e3:9.1f} kB")
 

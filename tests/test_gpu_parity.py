@@ -366,3 +366,54 @@ def test_c2_backward_vs_oracle(c2_case):
     g_g = R.rasterize_backward(st_g, R.ImageGradients(rgb=d_rgb))
     for k in O.GRAD_CLASSES:
         assert G.norm_rel(getattr(g_g, k), g_o[k]) <= GRAD_REL_F32, (k, G.norm_rel(getattr(g_g, k), g_o[k]))
+
+
+# -- densify / prune (train.py:237-284) vs the reference ------------------------------------
+
+def test_densify_and_prune_matches_reference():
+    from paper_2504_13339_b200.model import GaussianSet, PARAM_CLASSES
+    from paper_2504_13339_b200.train import DensifyStats, OptimizerState, TrainConfig, densify_and_prune
+
+    d = G.load("densify")
+    gs = GaussianSet(**{k: d["in_" + k].copy() for k in PARAM_CLASSES})
+    opt = OptimizerState(m={k: d["in_m_" + k].copy() for k in PARAM_CLASSES},
+                         v={k: d["in_v_" + k].copy() for k in PARAM_CLASSES})
+    st = DensifyStats(grad_accum=d["stats_grad"].copy(), pos_accum=d["stats_pos"].copy(),
+                      count=d["stats_count"].copy())
+    out = densify_and_prune(gs, opt, st, TrainConfig(iterations=100), 3.0, np.random.default_rng(7), 1e-3)
+    assert len(out) == len(d["out_position"])
+    for k in PARAM_CLASSES:
+        ref = d["out_" + k]
+        assert np.abs(getattr(out, k) - ref).max() <= 1e-12 * max(np.abs(ref).max(), 1.0), k
+        assert np.array_equal(opt.m[k], d["out_m_" + k]) and np.array_equal(opt.v[k], d["out_v_" + k]), k
+    assert len(st.count) == len(out) and not st.count.any()
+
+
+def test_trainer_densify_tracks_stats_and_resizes():
+    from paper_2504_13339_b200 import scenes
+    from paper_2504_13339_b200.device import DeviceTF
+    from paper_2504_13339_b200.train import Trainer, TrainConfig, View
+
+    learned = scenes.random_gaussians(3000, seed=0)
+    truth = scenes.random_gaussians(3000, seed=1)
+    tf = scenes.random_tf(2, 4)
+    cams = scenes.orbit_cameras(2, 3, 96, 96)
+    dtf = DeviceTF(tf)
+    from paper_2504_13339_b200.device import Rasterizer
+
+    rz = Rasterizer(pooled=False)
+    gt = torch.from_numpy(truth.pack()).cuda()
+    targets = [rz.forward(gt, len(truth), dtf, c).out_img.view(96, 96, 3).clone() for c in cams]
+    cfg = TrainConfig(iterations=100, densify_grad_threshold=1e-6)
+    tr = Trainer(learned, cfg)
+    tr.track_densify()
+    views = [View(c, dtf, t) for c, t in zip(cams, targets)]
+    for _ in range(3):
+        tr.step(views)
+    st = tr.densify_stats.view(-1, 5).cpu().numpy()
+    assert st[:, 4].max() == 6.0 and (st[:, 0] > 0).any()  # 3 steps x 2 views
+    n_before = tr.n
+    n_after = tr.densify_and_prune(3.0, np.random.default_rng(0), 1e-4)
+    assert n_after != n_before and tr.params.numel() == 19 * n_after
+    loss = tr.step(views)  # the resized set keeps training
+    assert torch.isfinite(loss)
