@@ -58,6 +58,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--render-frames", type=int, default=5)
     ap.add_argument("--cpu-budget-s", type=float, default=60.0)
+    ap.add_argument("--no-sweep", action="store_true", help="skip the config-3 TF-sweep render measurement")
+    ap.add_argument("--sweep-frames", type=int, default=2)
     return ap.parse_args()
 
 
@@ -300,6 +302,8 @@ def run_b200(args) -> None:
                    "avg_instances": sum(c[1] for c in v["counts"]) / len(v["counts"])}
                for k, v in ksum.items()}
 
+    sweep = None if args.no_sweep else run_sweep(args, dev, rank, world)
+
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline_sample(learned, tf, cams[mine[0]], targets[0].cpu().numpy(), args.cpu_budget_s)
@@ -308,11 +312,54 @@ def run_b200(args) -> None:
             "warmup": max(args.warmup, 3), "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f32+f64", "data": "synthetic (seeded, scenes.py)",
             "config": config_block(world), "e2e": e2e, "render_mpx_s": render_mpx_s, "loss": loss_val,
-            "gpu_launches": int(launches), "roofline": roof, "kernels": kernels, "cpu_baseline": cpu,
+            "gpu_launches": int(launches), "roofline": roof, "kernels": kernels, "render_sweep_c3": sweep,
+            "cpu_baseline": cpu,
             "clocks": clk}
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def run_sweep(args, dev, rank, world) -> dict:
+    """Config 3: 3M Gaussians (64-blob shape), 1920x1080, 8 fresh TFs per frame, forward
+    only; frames are sharded across ranks (replicas, no collective)."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2504_13339_b200 import scenes
+    from paper_2504_13339_b200.device import DeviceTF, Rasterizer
+
+    gs = scenes.blob_gaussians(3_000_000, seed=1)
+    params = torch.from_numpy(gs.pack()).to(dev)
+    n_frames = max(args.sweep_frames, 1) * world
+    cams = scenes.orbit_cameras(n_frames, 5, 1920, 1080)
+    mine = [f for f in range(n_frames) if f % world == rank]
+    tfs = {f: [DeviceTF(scenes.random_tf(1000 + 8 * f + k), dev) for k in range(8)] for f in mine}
+    rz = Rasterizer(pooled=True)
+    for tf in tfs[mine[0]][:2]:
+        rz.forward(params, len(gs), tf, cams[mine[0]])
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    inst = 0
+    for f in mine:
+        for tf in tfs[f]:
+            fr = rz.forward(params, len(gs), tf, cams[f])
+            inst += fr.n_inst
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    if world > 1:
+        t = torch.tensor([ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    renders = 8 * n_frames
+    return {"workload": "c3: 3M blob-shaped Gaussians, 1920x1080, 8 random 256-knot TFs per frame (1-6 bumps), "
+                        "forward render per (frame, TF), frames sharded across ranks",
+            "renders": renders, "ms_per_render": ms / (renders / world), "mpx_s": renders * 1920 * 1080 / (ms / 1e3) / 1e6,
+            "tf_frames_per_s": renders / (ms / 1e3), "avg_instances": inst / max(len(mine) * 8, 1)}
 
 
 # -- the CPU arm (oracle restatement of the reference algorithm) -------------------------

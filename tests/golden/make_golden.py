@@ -66,6 +66,10 @@ def to_ref_cam(vs, mine):
                             width=mine.width, height=mine.height, near=mine.near, far=mine.far)
 
 
+def importlib_model(vs):
+    return sys.modules["vegsplat.model"]
+
+
 def replay_contributors(b, clamp, stop):
     """Contributor count per pixel by replaying kernels.py:56-93 on the BlendState."""
     h, w = b.height, b.width
@@ -308,6 +312,23 @@ def main():
     dd.update({"out_m_" + k: v for k, v in opt.m.items()})
     dd.update({"out_v_" + k: v for k, v in opt.v.items()})
     save("densify", dd)
+
+    # -- VEGS model files written by the reference (model.py:236-282)
+    import tempfile
+
+    vm = importlib_model(vs)
+    with tempfile.TemporaryDirectory() as td:
+        small_gs = to_ref_gs(vs, scenes.random_gaussians(300, seed=51))
+        vm.save_model(small_gs, f"{td}/m.vegs")
+        vq = vm.vq_compress(small_gs, k=16, iters=4, seed=0)
+        vm.save_vq_model(vq, f"{td}/q.vegs")
+        vqd = vm.load_model(f"{td}/q.vegs")  # decompressed from the file (f32 payload)
+        mio = {"plain_bytes": np.frombuffer(open(f"{td}/m.vegs", "rb").read(), dtype=np.uint8),
+               "vq_bytes": np.frombuffer(open(f"{td}/q.vegs", "rb").read(), dtype=np.uint8)}
+        mio.update({"in_" + k: np.array(v) for k, v in small_gs.arrays().items()})
+        mio.update({"plain_" + k: np.array(v) for k, v in vm.load_model(f"{td}/m.vegs").arrays().items()})
+        mio.update({"vq_" + k: np.array(v) for k, v in vqd.arrays().items()})
+    save("model_io", mio)
 
     for k, v in saved.items():
         print(f"{k:20s} {v / 1e3:9.1f} kB")
