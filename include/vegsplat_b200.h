@@ -20,7 +20,8 @@
  *                               rows written in duplicate order for the deterministic reduction)
  *   vegs_preprocess_backward    raster/pipeline.py:307-366 (np.add.at reduction, project_backward
  *                               projection.py:186-277, shade_backward shading.py:97-176, GradientSet)
- *   vegs_loss_l1_ssim           loss.py:80-168 ssim / ssim_backward / compute_loss (regularisers off)
+ *   vegs_loss_l1_ssim           loss.py:80-168 ssim / ssim_backward / compute_loss (L1 + SSIM part)
+ *   vegs_loss_aux               loss.py:175-240 normal-consistency + bilateral-smoothness regularisers
  *   vegs_adam_step              train.py:176-195 adam_step (+ learning_rates :156-173 on the host)
  *   vegs_tf_eval                transfer.py:91-127 eval_opacity / eval_color / d_*_dv
  *   vegs_densify_count / _apply train.py:237-284 densify_and_prune (+ DensifyStats.add :210-214,
@@ -213,12 +214,21 @@ int vegs_densify_apply(const double *params, const double *m, const double *v, i
                        double *out_m, double *out_v, void *stream);
 
 /* ---- loss / optimiser ------------------------------------------------------------- */
-/* (w_l1) * mean|x - y| + lam * (1 - mean SSIM) on H x W x 3 float32 images; writes
- * d_x (H x W x 3 float32) and accumulates {sum |x-y|, sum ssim_map} into sums[2]
- * (float64, caller zeroes).  ws holds the SSIM gradient maps. */
-int vegs_loss_l1_ssim(const float *x, const float *y, int32_t height, int32_t width,
+/* (w_l1) * mean|x - y| + lam * (1 - mean SSIM) on the rgb channels of x (H x W x
+ * x_stride float32, rgb first; 3 for plain images, 11 for aux planes) against y (H x W x 3);
+ * writes the rgb channels of d_x (same layout as x) and accumulates {sum |x-y|,
+ * sum ssim_map} into sums[2] (float64, caller zeroes).  ws holds the SSIM gradient maps. */
+int vegs_loss_l1_ssim(const float *x, const float *y, int32_t height, int32_t width, int32_t x_stride,
                       double w_l1, double lam, float *d_x, double *sums, void *ws,
                       size_t *ws_bytes, void *stream);
+
+/* Aux-plane regularisers (loss.py:175-240) on planes (H x W x 11: rgb, depth, normal,
+ * attrs) with alpha = 1 - out_t: writes channels 3..10 of d_planes and accumulates
+ * {normal sum (1 - dot), mask count, smooth sum} into sums[3] (float64, caller zeroes).
+ * w_normal = 0 / w_smooth = 0 switch a term off (its gradient channels are written 0). */
+int vegs_loss_aux(const float *planes, const float *out_t, const float *ref_rgb, int32_t height,
+                  int32_t width, double px_scale, double w_normal, double w_smooth, float *d_planes,
+                  double *sums, void *ws, size_t *ws_bytes, void *stream);
 
 /* In-place bias-corrected Adam over the flat class-major float64 buffers (19 n).
  * lr[10] per class, grad_scale multiplies g first, bias1/bias2 = 1 - beta^t.

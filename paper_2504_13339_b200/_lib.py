@@ -70,7 +70,8 @@ _SIGS = {
                            c_int64, c_double, c_double, P, P, P, P, P],
     "vegs_blend_backward": [P, P, c_int64, c_int64, c_int64, P, P, P, P, P, P, c_int32, c_int32, P, c_int64,
                             c_int64, c_double, P, P, P, P, P, P, P, P, P],
-    "vegs_loss_l1_ssim": [P, P, c_int32, c_int32, c_double, c_double, P, P, P, POINTER(c_size_t), P],
+    "vegs_loss_l1_ssim": [P, P, c_int32, c_int32, c_int32, c_double, c_double, P, P, P, POINTER(c_size_t), P],
+    "vegs_loss_aux": [P, P, P, c_int32, c_int32, c_double, c_double, c_double, P, P, P, POINTER(c_size_t), P],
     "vegs_adam_step": [P, P, P, P, c_int64, P, c_double, c_double, c_double, P, P],
 }
 

@@ -35,8 +35,8 @@ __device__ __forceinline__ float block_sum_f(float v, float *red) {
 }
 
 __global__ void __launch_bounds__(256) ssim_fwd_kernel(const float *__restrict__ x, const float *__restrict__ y,
-                                                       int H, int W, Taps taps, float c1, float c2, float coeff,
-                                                       float *__restrict__ maps, double *sums) {
+                                                       int H, int W, int xs, Taps taps, float c1, float c2,
+                                                       float coeff, float *__restrict__ maps, double *sums) {
     __shared__ float sx[kIn][kIn + 1], sy[kIn][kIn + 1];
     __shared__ float hs[5][kIn][kLT + 1];
     __shared__ float red[8];
@@ -50,7 +50,7 @@ __global__ void __launch_bounds__(256) ssim_fwd_kernel(const float *__restrict__
             const int r = i / kIn, q = i - r * kIn;
             const int gy = u0 + r, gx = v0 + q;
             const bool ok = gy < H && gx < W;
-            sx[r][q] = ok ? x[((int64_t)gy * W + gx) * 3 + c] : 0.f;
+            sx[r][q] = ok ? x[((int64_t)gy * W + gx) * xs + c] : 0.f;
             sy[r][q] = ok ? y[((int64_t)gy * W + gx) * 3 + c] : 0.f;
         }
         __syncthreads();
@@ -106,7 +106,7 @@ __global__ void __launch_bounds__(256) ssim_fwd_kernel(const float *__restrict__
 }
 
 __global__ void __launch_bounds__(256) ssim_bwd_kernel(const float *__restrict__ x, const float *__restrict__ y,
-                                                       int H, int W, Taps taps, float l1_coeff,
+                                                       int H, int W, int xs, Taps taps, float l1_coeff,
                                                        const float *__restrict__ maps, float *__restrict__ dx,
                                                        double *sums) {
     __shared__ float sm[3][kIn][kIn + 1];
@@ -152,8 +152,9 @@ __global__ void __launch_bounds__(256) ssim_bwd_kernel(const float *__restrict__
 #pragma unroll
                 for (int e = 0; e < 3; ++e) acc[e] += k * hs[e][r + t][q];
             }
-            const int64_t p = ((int64_t)gi * W + gj) * 3 + c;
-            const float xv = x[p], yv = y[p];
+            const int64_t pix = (int64_t)gi * W + gj;
+            const int64_t p = pix * xs + c;
+            const float xv = x[p], yv = y[pix * 3 + c];
             const float d = xv - yv;
             l1 += fabsf(d);
             const float sgn = d > 0.f ? 1.f : (d < 0.f ? -1.f : 0.f);
@@ -168,9 +169,10 @@ __global__ void __launch_bounds__(256) ssim_bwd_kernel(const float *__restrict__
 
 using namespace vegs;
 
-extern "C" int vegs_loss_l1_ssim(const float *x, const float *y, int32_t height, int32_t width, double w_l1,
-                                 double lam, float *d_x, double *sums, void *ws, size_t *ws_bytes, void *stream) {
-    if (!ws_bytes || height < kWin || width < kWin) return VEGS_ERR_ARG;
+extern "C" int vegs_loss_l1_ssim(const float *x, const float *y, int32_t height, int32_t width, int32_t x_stride,
+                                 double w_l1, double lam, float *d_x, double *sums, void *ws, size_t *ws_bytes,
+                                 void *stream) {
+    if (!ws_bytes || height < kWin || width < kWin || x_stride < 3) return VEGS_ERR_ARG;
     const int64_t Hv = height - 2 * kHalf, Wv = width - 2 * kHalf;
     const size_t need = sizeof(float) * 9 * (size_t)(Hv * Wv);
     if (!ws) {
@@ -194,10 +196,165 @@ extern "C" int vegs_loss_l1_ssim(const float *x, const float *y, int32_t height,
     const float l1c = (float)(w_l1 / ((double)height * width * 3.0));
     cudaStream_t s = (cudaStream_t)stream;
     dim3 g1((unsigned)((Wv + kLT - 1) / kLT), (unsigned)((Hv + kLT - 1) / kLT));
-    ssim_fwd_kernel<<<g1, 256, 0, s>>>(x, y, height, width, taps, c1, c2, coeff, (float *)ws, sums);
+    ssim_fwd_kernel<<<g1, 256, 0, s>>>(x, y, height, width, x_stride, taps, c1, c2, coeff, (float *)ws, sums);
     VEGS_CHECK_LAUNCH();
     dim3 g2((unsigned)((width + kLT - 1) / kLT), (unsigned)((height + kLT - 1) / kLT));
-    ssim_bwd_kernel<<<g2, 256, 0, s>>>(x, y, height, width, taps, l1c, (const float *)ws, d_x, sums);
+    ssim_bwd_kernel<<<g2, 256, 0, s>>>(x, y, height, width, x_stride, taps, l1c, (const float *)ws, d_x, sums);
+    VEGS_CHECK_LAUNCH();
+    return VEGS_OK;
+}
+
+// ---- auxiliary-plane regularisers (loss.py:175-240) -------------------------------------
+// planes: (H, W, 11) = rgb, depth, normal(3), attrs(4); alpha = 1 - T.  Normal consistency
+// compares the blended normal with a depth-derived pseudo-normal on interior pixels with
+// alpha > 0.5 (mask detached); bilateral smoothness penalises attr-plane differences
+// weighted by exp(-|d ref_gray|).  sums += {normal sum (1-dot), mask count, smooth sum}.
+
+namespace vegs {
+
+__device__ __forceinline__ bool normal_mask(const float *T, int H, int W, int y, int x) {
+    return y > 0 && x > 0 && y < H - 1 && x < W - 1 && (1.f - T[(int64_t)y * W + x]) > 0.5f;
+}
+
+__global__ void normal_count_kernel(const float *T, int H, int W, double *sums) {
+    __shared__ float red[8];
+    float c = 0.f;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < (int64_t)H * W;
+         i += (int64_t)gridDim.x * blockDim.x)
+        c += normal_mask(T, H, W, (int)(i / W), (int)(i % W)) ? 1.f : 0.f;
+    const float tot = block_sum_f(c, red);
+    if (threadIdx.x == 0) atomicAdd(sums + 1, (double)tot);
+}
+
+// per pixel: d normal, the normal term, and g_nd_raw (3 floats) for the depth gather
+__global__ void normal_pass_kernel(const float *P, const float *T, int H, int W, float px_scale, float w_n,
+                                   double *sums, float *g_raw, float *dP) {
+    __shared__ float red[8];
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    float term = 0.f;
+    if (i < (int64_t)H * W) {
+        const int y = (int)(i / W), x = (int)(i % W);
+        float g3[3] = {0.f, 0.f, 0.f};
+        float dn[3] = {0.f, 0.f, 0.f};
+        if (normal_mask(T, H, W, y, x)) {
+            const float cnt = (float)sums[1];
+            const float *p = P + i * 11;
+            const float gx = 0.5f * (P[(i + 1) * 11 + 3] - P[(i - 1) * 11 + 3]);
+            const float gy = 0.5f * (P[(i + W) * 11 + 3] - P[(i - W) * 11 + 3]);
+            const float nd[3] = {-gx, -gy, px_scale * p[3]};
+            const float ndl = fmaxf(sqrtf(nd[0] * nd[0] + nd[1] * nd[1] + nd[2] * nd[2]), 1e-12f);
+            const float nrl = fmaxf(sqrtf(p[4] * p[4] + p[5] * p[5] + p[6] * p[6]), 1e-12f);
+            float ndh[3], nrh[3], dot = 0.f;
+            for (int k = 0; k < 3; ++k) {
+                ndh[k] = nd[k] / ndl;
+                nrh[k] = p[4 + k] / nrl;
+                dot += nrh[k] * ndh[k];
+            }
+            term = 1.f - dot;
+            const float sc = -w_n / cnt;
+            float pr = 0.f, pd = 0.f;
+            for (int k = 0; k < 3; ++k) {
+                pr += sc * ndh[k] * nrh[k];
+                pd += sc * nrh[k] * ndh[k];
+            }
+            for (int k = 0; k < 3; ++k) {
+                dn[k] = (sc * ndh[k] - pr * nrh[k]) / nrl;
+                g3[k] = (sc * nrh[k] - pd * ndh[k]) / ndl;
+            }
+        }
+        for (int k = 0; k < 3; ++k) {
+            g_raw[i * 3 + k] = g3[k];
+            dP[i * 11 + 4 + k] = dn[k];
+        }
+    }
+    const float tot = block_sum_f(term, red);
+    if (threadIdx.x == 0) atomicAdd(sums, (double)tot);
+}
+
+__device__ __forceinline__ float gray(const float *ref, int64_t i) {
+    return (fabsf(ref[i * 3]) + fabsf(ref[i * 3 + 1]) + fabsf(ref[i * 3 + 2])) / 3.f;
+}
+
+// depth gradient (gather of the neighbours' pseudo-normal terms) + attr smoothness
+__global__ void aux_gather_kernel(const float *P, const float *ref, const float *g_raw, int H, int W, float px_scale,
+                                  float w_s, int smooth, float *dP, double *sums) {
+    __shared__ float red[8];
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    float acc = 0.f;
+    if (i < (int64_t)H * W) {
+        const int y = (int)(i / W), x = (int)(i % W);
+        // nd_raw = (-gx, -gy, s z): d z[y,x] = s g_z + 0.5 (g_gx(x-1) - g_gx(x+1) + g_gy(y-1) - g_gy(y+1)),
+        // g_gx = -g_raw_x, g_gy = -g_raw_y
+        float dz = px_scale * g_raw[i * 3 + 2];
+        if (x > 0) dz += -0.5f * g_raw[(i - 1) * 3 + 0];
+        if (x < W - 1) dz -= -0.5f * g_raw[(i + 1) * 3 + 0];
+        if (y > 0) dz += -0.5f * g_raw[(i - W) * 3 + 1];
+        if (y < H - 1) dz -= -0.5f * g_raw[(i + W) * 3 + 1];
+        dP[i * 11 + 3] = dz;
+        float da[4] = {0.f, 0.f, 0.f, 0.f};
+        if (smooth) {
+            const float n_terms = 4.f * ((float)H * (W - 1) + (float)(H - 1) * W);
+            const float g0 = gray(ref, i);
+            const float ex_r = x < W - 1 ? expf(-fabsf(gray(ref, i + 1) - g0)) : 0.f;   // edge (x, x+1)
+            const float ex_l = x > 0 ? expf(-fabsf(g0 - gray(ref, i - 1))) : 0.f;       // edge (x-1, x)
+            const float ey_d = y < H - 1 ? expf(-fabsf(gray(ref, i + W) - g0)) : 0.f;   // edge (y, y+1)
+            const float ey_u = y > 0 ? expf(-fabsf(g0 - gray(ref, i - W))) : 0.f;       // edge (y-1, y)
+            for (int k = 0; k < 4; ++k) {
+                const float a0 = P[i * 11 + 7 + k];
+                if (x < W - 1) {
+                    const float d = P[(i + 1) * 11 + 7 + k] - a0;
+                    acc += fabsf(d) * ex_r;
+                    da[k] -= w_s * (d > 0.f ? 1.f : (d < 0.f ? -1.f : 0.f)) * ex_r / n_terms;
+                }
+                if (x > 0) {
+                    const float d = a0 - P[(i - 1) * 11 + 7 + k];
+                    da[k] += w_s * (d > 0.f ? 1.f : (d < 0.f ? -1.f : 0.f)) * ex_l / n_terms;
+                }
+                if (y < H - 1) {
+                    const float d = P[(i + W) * 11 + 7 + k] - a0;
+                    acc += fabsf(d) * ey_d;
+                    da[k] -= w_s * (d > 0.f ? 1.f : (d < 0.f ? -1.f : 0.f)) * ey_d / n_terms;
+                }
+                if (y > 0) {
+                    const float d = a0 - P[(i - W) * 11 + 7 + k];
+                    da[k] += w_s * (d > 0.f ? 1.f : (d < 0.f ? -1.f : 0.f)) * ey_u / n_terms;
+                }
+            }
+        }
+        for (int k = 0; k < 4; ++k) dP[i * 11 + 7 + k] = da[k];
+    }
+    const float tot = block_sum_f(acc, red);
+    if (threadIdx.x == 0) atomicAdd(sums + 2, (double)tot);
+}
+
+}  // namespace vegs
+
+extern "C" int vegs_loss_aux(const float *planes, const float *out_t, const float *ref_rgb, int32_t height,
+                             int32_t width, double px_scale, double w_normal, double w_smooth, float *d_planes,
+                             double *sums, void *ws, size_t *ws_bytes, void *stream) {
+    if (!ws_bytes || height < 3 || width < 3) return VEGS_ERR_ARG;
+    const int64_t hw = (int64_t)height * width;
+    const size_t need = sizeof(float) * 3 * (size_t)hw;
+    if (!ws) {
+        *ws_bytes = need;
+        return VEGS_OK;
+    }
+    if (*ws_bytes < need) return VEGS_ERR_CAPACITY;
+    if (!planes || !out_t || !ref_rgb || !d_planes || !sums) return VEGS_ERR_ARG;
+    cudaStream_t s = (cudaStream_t)stream;
+    const int blocks = (int)((hw + 255) / 256);
+    float *g_raw = (float *)ws;
+    if (w_normal > 0.0) {
+        normal_count_kernel<<<148 * 4, 256, 0, s>>>(out_t, height, width, sums);
+        VEGS_CHECK_LAUNCH();
+        normal_pass_kernel<<<blocks, 256, 0, s>>>(planes, out_t, height, width, (float)px_scale, (float)w_normal,
+                                                  sums, g_raw, d_planes);
+    } else {
+        VEGS_CUDA(cudaMemsetAsync(g_raw, 0, need, s));
+    }
+    VEGS_CHECK_LAUNCH();
+    aux_gather_kernel<<<blocks, 256, 0, s>>>(planes, ref_rgb, g_raw, height, width, (float)px_scale, (float)w_smooth,
+                                             w_smooth > 0.0 ? 1 : 0, d_planes, sums);
     VEGS_CHECK_LAUNCH();
     return VEGS_OK;
 }

@@ -43,6 +43,7 @@ LAUNCHES = {
     "vegs_composite_backward": 1,
     "vegs_preprocess_backward": 2,  # row reduction + chain
     "vegs_loss_l1_ssim": 2,
+    "vegs_loss_aux": 3,
     "vegs_adam_step": 1,
     "vegs_densify_count": 3,
     "vegs_densify_apply": 1,
@@ -335,7 +336,8 @@ def tf_eval(ts, vals, v, derivative: bool) -> np.ndarray:
 
 
 class LossKernel:
-    """Fused L1 + SSIM forward/backward (vegs_loss_l1_ssim) with a reusable workspace."""
+    """Fused L1 + SSIM forward/backward (vegs_loss_l1_ssim) and the aux-plane regularisers
+    (vegs_loss_aux), with reusable workspaces."""
 
     def __init__(self, device=None):
         self.device = device or require_cuda()
@@ -343,12 +345,22 @@ class LossKernel:
 
     def __call__(self, x: torch.Tensor, y: torch.Tensor, w_l1: float, lam: float, d_x: torch.Tensor,
                  sums: torch.Tensor) -> None:
-        h, w = int(x.shape[0]), int(x.shape[1])
-        nbytes = _lib.size_query("vegs_loss_l1_ssim", _p(x), _p(y), h, w, float(w_l1), float(lam), _p(d_x),
+        """x: (H, W, S) float32 with rgb in channels 0..2 (S = 3 or 11); y: (H, W, 3)."""
+        h, w, xs = int(x.shape[0]), int(x.shape[1]), int(x.shape[2])
+        nbytes = _lib.size_query("vegs_loss_l1_ssim", _p(x), _p(y), h, w, xs, float(w_l1), float(lam), _p(d_x),
                                  _p(sums), tail=(_stream(),))
         ws = self.pool.get("ws", nbytes, torch.uint8)
-        call("vegs_loss_l1_ssim", _p(x), _p(y), h, w, float(w_l1), float(lam), _p(d_x), _p(sums), _p(ws),
+        call("vegs_loss_l1_ssim", _p(x), _p(y), h, w, xs, float(w_l1), float(lam), _p(d_x), _p(sums), _p(ws),
              ctypes.byref(ctypes.c_size_t(nbytes)), _stream())
+
+    def aux(self, planes: torch.Tensor, out_t: torch.Tensor, ref: torch.Tensor, px_scale: float, w_normal: float,
+            w_smooth: float, d_planes: torch.Tensor, sums3: torch.Tensor) -> None:
+        h, w = int(planes.shape[0]), int(planes.shape[1])
+        nbytes = _lib.size_query("vegs_loss_aux", _p(planes), _p(out_t), _p(ref), h, w, float(px_scale),
+                                 float(w_normal), float(w_smooth), _p(d_planes), _p(sums3), tail=(_stream(),))
+        ws = self.pool.get("ws_aux", nbytes, torch.uint8)
+        call("vegs_loss_aux", _p(planes), _p(out_t), _p(ref), h, w, float(px_scale), float(w_normal),
+             float(w_smooth), _p(d_planes), _p(sums3), _p(ws), ctypes.byref(ctypes.c_size_t(nbytes)), _stream())
 
 
 def adam_step_device(params, grads, m, v, n: int, lrs: torch.Tensor, grad_scale: float, step: int,

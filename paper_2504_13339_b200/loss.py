@@ -7,9 +7,10 @@ K2 0.03) over valid positions, and its exact analytic adjoint
 ``L1 + 0.2 (1 - SSIM)`` while the reference weights L1 by (1 - lambda); ``compute_loss``
 keeps the reference's convention and ``l1_weight`` selects the other.
 
-The normal-consistency and bilateral-smoothness regularisers (loss.py:175-240) are
-not on the measured path (their weights are 0 in every BASELINE config); asking for
-them raises ``NotImplementedError`` instead of silently dropping them.
+The normal-consistency and bilateral-smoothness regularisers (loss.py:175-240) run in
+``vegs_loss_aux`` on the auxiliary planes (depth, normal, attrs) when the rendered
+buffer carries them, exactly as the reference applies them (weights from the config;
+0 in every BASELINE config).
 """
 
 from __future__ import annotations
@@ -49,7 +50,7 @@ def l1_ssim_device(x: torch.Tensor, y: torch.Tensor, w_l1: float, lam: float,
                    d_x: torch.Tensor | None = None, sums: torch.Tensor | None = None):
     """Device entry: x, y float32 (H, W, 3) CUDA tensors.  Returns (d_x, sums) where
     sums = [sum |x - y|, sum SSIM map] (float64, accumulated into if given)."""
-    if x.shape != y.shape or x.dim() != 3 or x.shape[2] != 3:
+    if x.shape[:2] != y.shape[:2] or x.dim() != 3 or x.shape[2] < 3 or y.shape[2] != 3:
         raise ValueError(f"rendered {tuple(x.shape)} vs reference {tuple(y.shape)}")
     if x.shape[0] < SSIM_WINDOW or x.shape[1] < SSIM_WINDOW:
         raise ValueError(f"images must be at least {SSIM_WINDOW}px for SSIM")
@@ -106,22 +107,55 @@ class LossBreakdown:
 
 def compute_loss(rendered: ImageBuffer, reference_rgb: np.ndarray, config, px_scale: float = 1.0,
                  l1_weight: float | None = None) -> tuple[float, ImageGradients, LossBreakdown]:
-    """Scalar loss and dL/d rgb (loss.py:146-168)."""
+    """Scalar loss and gradients for every rendered plane (loss.py:146-245)."""
     rgb = rendered.rgb
     if rgb.shape != np.shape(reference_rgb):
         raise ValueError(f"rendered {rgb.shape} vs reference {np.shape(reference_rgb)}")
-    if (getattr(config, "normal_loss_weight", 0.0) > 0.0 and rendered.normal is not None
-            and rendered.depth is not None) or (getattr(config, "smooth_loss_weight", 0.0) > 0.0
-                                               and rendered.attrs is not None):
-        raise NotImplementedError("normal/smoothness regularisers are outside the B200 hot path (SURVEY §8(f))")
     lam = float(config.lambda_ssim)
     w_l1 = (1.0 - lam) if l1_weight is None else float(l1_weight)
-    d_x, sums = l1_ssim_device(_to_dev(rgb), _to_dev(reference_rgb), w_l1, lam)
+    w_n = float(getattr(config, "normal_loss_weight", 0.0))
+    w_s = float(getattr(config, "smooth_loss_weight", 0.0))
+    use_n = w_n > 0.0 and rendered.normal is not None and rendered.depth is not None
+    use_s = w_s > 0.0 and rendered.attrs is not None
+    dev = require_cuda()
+    ref = _to_dev(reference_rgb)
+    h, w = rgb.shape[:2]
+    if use_n or use_s:  # one (H, W, 11) plane stack like the blend produces
+        planes = np.zeros((h, w, 11), dtype=np.float32)
+        planes[:, :, :3] = rgb
+        if rendered.depth is not None:
+            planes[:, :, 3] = rendered.depth
+        if rendered.normal is not None:
+            planes[:, :, 4:7] = rendered.normal
+        if rendered.attrs is not None:
+            planes[:, :, 7:11] = rendered.attrs
+        x = torch.from_numpy(planes).to(dev)
+    else:
+        x = _to_dev(rgb)
+    d_x = torch.zeros_like(x)
+    d_x, sums = l1_ssim_device(x, ref, w_l1, lam, d_x)
+    normal_term = smooth_term = 0.0
+    if use_n or use_s:
+        t = _to_dev(1.0 - np.asarray(rendered.alpha, dtype=np.float32)).contiguous()
+        sums3 = torch.zeros(3, dtype=torch.float64, device=dev)
+        _kernel().aux(x, t, ref, px_scale, w_n if use_n else 0.0, w_s if use_s else 0.0, d_x, sums3)
+        s3 = sums3.cpu().numpy()
+        if use_n and s3[1] > 0:
+            normal_term = w_n * float(s3[0]) / float(s3[1])
+        if use_s:
+            smooth_term = w_s * float(s3[2]) / (4 * (h * (w - 1) + (h - 1) * w))
     n_el = rgb.size
-    n_pos = (rgb.shape[0] - 10) * (rgb.shape[1] - 10) * rgb.shape[2]
+    n_pos = (h - 10) * (w - 10) * 3
     s = sums.cpu().numpy()
     l1 = float(s[0]) / n_el
     ssim_term = 1.0 - float(s[1]) / n_pos
-    total = w_l1 * l1 + lam * ssim_term
-    grads = ImageGradients(rgb=d_x.cpu().numpy().astype(rgb.dtype))
-    return total, grads, LossBreakdown(total=total, l1=l1, ssim_term=ssim_term, normal=0.0, smooth=0.0)
+    total = w_l1 * l1 + lam * ssim_term + normal_term + smooth_term
+    dx = d_x.cpu().numpy()
+    grads = ImageGradients(rgb=np.ascontiguousarray(dx[:, :, :3]).astype(rgb.dtype))
+    if use_n:
+        grads.depth = np.ascontiguousarray(dx[:, :, 3]).astype(rgb.dtype)
+        grads.normal = np.ascontiguousarray(dx[:, :, 4:7]).astype(rgb.dtype)
+    if use_s:
+        grads.attrs = np.ascontiguousarray(dx[:, :, 7:11]).astype(rgb.dtype)
+    return total, grads, LossBreakdown(total=total, l1=l1, ssim_term=ssim_term, normal=normal_term,
+                                       smooth=smooth_term)

@@ -170,7 +170,7 @@ class Trainer:
     GPUs; the gradient buffer is all-reduced once per step."""
 
     def __init__(self, gs: GaussianSet, config: TrainConfig, settings: RasterSettings = DEFAULT_SETTINGS,
-                 background=(1.0, 1.0, 1.0), l1_weight: float | None = None, group=None):
+                 background=(1.0, 1.0, 1.0), l1_weight: float | None = None, group=None, with_aux: bool = False):
         self.device = require_cuda()
         self.n = len(gs)
         self.config = config
@@ -183,7 +183,10 @@ class Trainer:
         self.grads = torch.zeros_like(self.params)
         self.nonfinite = torch.zeros(10, dtype=torch.int32, device=self.device)
         self.step_count = 0
-        self.rz = Rasterizer(settings, 3, store_f64=False, pooled=True)
+        # with_aux: blend the 11 planes (rgb, depth, normal, attrs) and apply the normal /
+        # smoothness regularisers, as the reference's loop does (train.py:476-479)
+        self.with_aux = with_aux
+        self.rz = Rasterizer(settings, 11 if with_aux else 3, store_f64=False, pooled=True)
         self.group = group
         self.densify_stats = None  # (n, 5) float64 when densification is tracked
         self._d_img = None
@@ -195,10 +198,17 @@ class Trainer:
     def accumulate_view(self, view: View, scale: float, first: bool, sums: torch.Tensor) -> None:
         fr = self.rz.forward(self.params, self.n, view.tf, view.camera, self.background)
         h, w = fr.height, fr.width
-        img = fr.out_img.view(h, w, 3)
+        img = fr.out_img.view(h, w, fr.n_ch)
         if self._d_img is None or self._d_img.numel() != img.numel():
             self._d_img = torch.empty_like(img)
-        l1_ssim_device(img, view.target, self.w_l1, self.lam, self._d_img, sums)
+        l1_ssim_device(img, view.target, self.w_l1, self.lam, self._d_img, sums[:2])
+        if self.with_aux:
+            from .loss import _kernel
+
+            cam = view.camera
+            px_scale = 2.0 * math.tan(0.5 * cam.fov_y) / cam.height
+            _kernel().aux(img, fr.out_t.view(h, w), view.target, px_scale, self.config.normal_loss_weight,
+                          self.config.smooth_loss_weight, self._d_img, sums[2:5])
         self.rz.backward(fr, self._d_img, None, self.grads, scale=scale, accumulate=not first,
                          densify_stats=self.densify_stats)
 
@@ -207,7 +217,7 @@ class Trainer:
         """One optimisation step over this rank's views; returns the mean loss over
         this rank's views as a device scalar (no host sync)."""
         total = total_views if total_views is not None else len(views)
-        sums = torch.zeros(len(views), 2, dtype=torch.float64, device=self.device)
+        sums = torch.zeros(len(views), 5, dtype=torch.float64, device=self.device)
         if not views:
             self.grads.zero_()
         for i, view in enumerate(views):
@@ -224,6 +234,11 @@ class Trainer:
         n_el = h * w * 3
         n_pos = (h - 10) * (w - 10) * 3
         per_view = self.w_l1 * sums[:, 0] / n_el + self.lam * (1.0 - sums[:, 1] / n_pos)
+        if self.with_aux:
+            cnt = sums[:, 3]
+            per_view = per_view + torch.where(cnt > 0, self.config.normal_loss_weight * sums[:, 2] / cnt.clamp(min=1),
+                                              torch.zeros_like(cnt))
+            per_view = per_view + self.config.smooth_loss_weight * sums[:, 4] / (4 * (h * (w - 1) + (h - 1) * w))
         return per_view.mean()
 
     def track_densify(self, on: bool = True) -> None:

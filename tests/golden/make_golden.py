@@ -237,6 +237,26 @@ def main():
                    f"{name}_grad": grads.rgb})
     save("loss", ld)
 
+    # -- loss with the auxiliary-plane regularisers on (loss.py:175-240), float32 planes
+    class CfgAux:
+        lambda_ssim = 0.2
+        normal_loss_weight = 0.01
+        smooth_loss_weight = 0.001
+
+    rng_a = np.random.default_rng(23)
+    h_a, w_a = 30, 34
+    buf = dict(rgb=rng_a.uniform(0.05, 0.95, size=(h_a, w_a, 3)).astype(np.float32),
+               alpha=np.where(rng_a.uniform(size=(h_a, w_a)) < 0.8, 0.9, 0.2).astype(np.float32),
+               depth=(3.0 + rng_a.uniform(0, 1, size=(h_a, w_a))).astype(np.float32),
+               normal=(rng_a.uniform(-1, 1, size=(h_a, w_a, 3)) + np.array([0.0, 0.0, 2.0])).astype(np.float32),
+               attrs=rng_a.uniform(0.1, 0.9, size=(h_a, w_a, 4)).astype(np.float32))
+    ref_a = rng_a.uniform(0, 1, size=(h_a, w_a, 3)).astype(np.float32)
+    tot_a, g_a, br_a = vs.loss.compute_loss(vs.images.ImageBuffer(**buf), ref_a, CfgAux(), px_scale=0.01)
+    la = {"in_" + k: v for k, v in buf.items()}
+    la.update(ref=ref_a, total=np.array(tot_a), normal_term=np.array(br_a.normal), smooth_term=np.array(br_a.smooth),
+              g_rgb=g_a.rgb, g_depth=g_a.depth, g_normal=g_a.normal, g_attrs=g_a.attrs)
+    save("loss_aux", la)
+
     # -- Adam with per-class learning rates (train.py:156-195), 3 steps
     cfg = vtrain.TrainConfig(iterations=100)
     ga = scenes.random_gaussians(64, seed=31)
@@ -287,6 +307,31 @@ def main():
     ts.update({"out_" + k: np.array(v) for k, v in rl.arrays().items()})
     ts["losses"] = np.array(losses)
     save("train_step", ts)
+
+    # -- the reference's own training iteration with aux planes + regularisers on
+    #    (train.py:476-483, TrainConfig defaults: normal 0.01, smooth 0.001), 2 views
+    cfg_aux = vtrain.TrainConfig(iterations=100)
+    rl = to_ref_gs(vs, learned)
+    tsa, tot, losses = {}, None, []
+    for v_i, c in enumerate(cams2):
+        rc = to_ref_cam(vs, c)
+        target = vs.raster.render(rt, rtf, rc, (1.0, 1.0, 1.0), dtype=np.float32).rgb
+        img, st = vs.raster.render_with_state(rl, rtf, rc, (1.0, 1.0, 1.0), with_aux=True, dtype=np.float32)
+        px_scale = 2.0 * math.tan(0.5 * rc.fov_y) / rc.height
+        loss, ig, _ = vs.loss.compute_loss(img, target, cfg_aux, px_scale=px_scale)
+        losses.append(loss)
+        g = vs.raster.rasterize_backward(st, ig)
+        tsa[f"target{v_i}"] = target
+        tot = {k: v.copy() for k, v in g.arrays().items()} if tot is None else {k: tot[k] + v for k, v in g.arrays().items()}
+    mean = vs.raster.GradientSet.zeros(len(rl))
+    for k, v in mean.arrays().items():
+        v[...] = tot[k] / len(cams2)
+        tsa["grad_" + k] = v.copy()
+    opt = vtrain.OptimizerState.for_set(rl)
+    vtrain.adam_step(rl, mean, opt, cfg_aux, 1)
+    tsa.update({"out_" + k: np.array(v) for k, v in rl.arrays().items()})
+    tsa["losses"] = np.array(losses)
+    save("train_step_aux", tsa)
 
     # -- densify / prune (train.py:237-284): clones, splits (seeded rng) and weight pruning
     rng_d = np.random.default_rng(42)

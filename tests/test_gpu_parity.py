@@ -417,3 +417,46 @@ def test_trainer_densify_tracks_stats_and_resizes():
     assert n_after != n_before and tr.params.numel() == 19 * n_after
     loss = tr.step(views)  # the resized set keeps training
     assert torch.isfinite(loss)
+
+
+# -- aux planes: regularisers and the reference's default training iteration ---------------
+
+def test_loss_with_regularisers_vs_reference():
+    from paper_2504_13339_b200.images import ImageBuffer
+    from paper_2504_13339_b200.loss import compute_loss
+
+    class CfgAux:
+        lambda_ssim = 0.2
+        normal_loss_weight = 0.01
+        smooth_loss_weight = 0.001
+
+    d = G.load("loss_aux")
+    buf = ImageBuffer(**{k: d["in_" + k] for k in ("rgb", "alpha", "depth", "normal", "attrs")})
+    total, g, br = compute_loss(buf, d["ref"], CfgAux(), px_scale=0.01)
+    assert abs(total - float(d["total"])) <= 1e-5 * abs(float(d["total"]))
+    assert abs(br.normal - float(d["normal_term"])) <= 1e-5 * abs(float(d["normal_term"]))
+    assert abs(br.smooth - float(d["smooth_term"])) <= 1e-5 * abs(float(d["smooth_term"]))
+    for k in ("rgb", "depth", "normal", "attrs"):
+        assert G.norm_rel(getattr(g, k), d["g_" + k]) <= 1e-4, k
+
+
+def test_trainer_aux_step_matches_reference_iteration():
+    from paper_2504_13339_b200 import scenes
+    from paper_2504_13339_b200.device import DeviceTF
+    from paper_2504_13339_b200.model import PARAM_CLASSES
+    from paper_2504_13339_b200.train import Trainer, TrainConfig, View
+
+    d = G.load("train_step_aux")
+    learned = scenes.random_gaussians(2000, seed=0)
+    tf = scenes.random_tf(2, 4)
+    cams = scenes.orbit_cameras(2, 3, 64, 64)
+    tr = Trainer(learned, TrainConfig(iterations=100), with_aux=True)
+    dtf = DeviceTF(tf)
+    views = [View(c, dtf, torch.from_numpy(d[f"target{i}"]).cuda()) for i, c in enumerate(cams)]
+    loss = float(tr.step(views, iteration=1).item())
+    assert abs(loss - float(np.mean(d["losses"]))) <= 1e-5 * abs(float(np.mean(d["losses"])))
+    out = tr.gaussians()
+    for k in PARAM_CLASSES:
+        step_ref = d["out_" + k] - getattr(learned, k)
+        step_gpu = getattr(out, k) - getattr(learned, k)
+        assert G.norm_rel(step_gpu, step_ref) <= 1e-3, k
