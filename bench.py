@@ -133,15 +133,16 @@ class KernelTimer:
         self.open: dict = {}
         self.done: dict = {n: [] for n in names}
 
-    def mark(self, name, begin):
+    def mark(self, name, begin, rz=None):
         if name not in self.names:
             return
         ev = self.torch.cuda.Event(enable_timing=True)
-        ev.record()
+        ev.record()  # on the current stream = the launching stream
+        key = (name, id(rz))
         if begin:
-            self.open[name] = (ev, self.rz.last_counts)
+            self.open[key] = (ev, (rz or self.rz).last_counts)
         else:
-            start, counts = self.open.pop(name)
+            start, counts = self.open.pop(key)
             self.done[name].append((start, ev, counts))
 
     def summary(self) -> dict:
@@ -214,8 +215,8 @@ def run_b200(args) -> None:
 
     # ---- timed region: device-resident training steps
     timer = KernelTimer(trainer.rz)
-    trainer.rz.timer = timer
-    launches0 = trainer.rz.launches
+    trainer.set_timer(timer)
+    launches0 = trainer.launches
     clocks = ClockSampler(local)
     barrier()
     torch.cuda.synchronize()
@@ -229,9 +230,9 @@ def run_b200(args) -> None:
     torch.cuda.synchronize()
     barrier()
     clk = clocks.stop()
-    trainer.rz.timer = None
+    trainer.set_timer(None)
     ms = max_over_ranks(e0.elapsed_time(e1))
-    launches = trainer.rz.launches - launches0 + args.steps * (2 * len(views) + 1)  # + loss, Adam
+    launches = trainer.launches - launches0 + args.steps * 1  # + Adam
     ms_step = ms / args.steps
     value = 1000.0 / ms_step
     ksum = timer.summary()

@@ -191,18 +191,21 @@ class Rasterizer:
 
     def _run(self, name: str, *args) -> None:
         if self.timer is not None:
-            self.timer.mark(name, True)
+            self.timer.mark(name, True, self)
         call(name, *args)
         if self.timer is not None:
-            self.timer.mark(name, False)
+            self.timer.mark(name, False, self)
         self.launches += LAUNCHES.get(name, 1)
 
     def _alloc(self):
         return self.pool if self.pool is not None else _Fresh(self.device)
 
     # -- forward --------------------------------------------------------------------
-    def forward(self, params: torch.Tensor, n: int, tf: DeviceTF, cam, background=(1.0, 1.0, 1.0),
-                want_order: bool = False, api_views: bool = False) -> Frame:
+    def forward_begin(self, params: torch.Tensor, n: int, tf: DeviceTF, cam, background=(1.0, 1.0, 1.0),
+                      want_order: bool = False, api_views: bool = False) -> dict:
+        """First half of a forward: preprocess + instance count, with the count copied to
+        pinned host memory asynchronously.  ``forward_end`` waits for it and finishes; a
+        caller can queue other streams' work in between (see Trainer)."""
         A = self._alloc()
         rs = rec_stride(self.n_ch)
         record = A.get("record", n * rs, self.real)
@@ -221,8 +224,12 @@ class Rasterizer:
         cs = camera_struct(cam)
         self._run("vegs_preprocess_forward", _p(params), n, ctypes.byref(cs), ctypes.byref(tf.struct),
              ctypes.byref(self.st), self.n_ch, int(self.store_f64), ctypes.byref(tab), _stream())
-        return self._bin_and_blend(A, n, record, rect, tiles, depth_key, cam.width, cam.height, background,
-                                   cs, tf, params, want_order, api)
+        return self._bin_begin(A, n, record, rect, tiles, depth_key, cam.width, cam.height, background, cs, tf,
+                               params, want_order, api)
+
+    def forward(self, params: torch.Tensor, n: int, tf: DeviceTF, cam, background=(1.0, 1.0, 1.0),
+                want_order: bool = False, api_views: bool = False) -> Frame:
+        return self.forward_end(self.forward_begin(params, n, tf, cam, background, want_order, api_views))
 
     def forward_from_splats(self, mean2d, conic, alpha_base, depth, rect, channels, width, height,
                             background, want_order: bool = True) -> Frame:
@@ -237,11 +244,11 @@ class Rasterizer:
         tab = VegsSplatTable(_p(record), _p(rect_d), _p(tiles), _p(depth_key))
         self._run("vegs_splat_table_from_arrays", _p(mean2d), _p(conic), _p(alpha_base), _p(depth), _p(rect),
              _p(channels), m, ctypes.byref(self.st), self.n_ch, int(self.store_f64), ctypes.byref(tab), _stream())
-        return self._bin_and_blend(A, m, record, rect_d, tiles, depth_key, width, height, background, None,
-                                   None, None, want_order, {})
+        return self.forward_end(self._bin_begin(A, m, record, rect_d, tiles, depth_key, width, height, background,
+                                                None, None, None, want_order, {}))
 
-    def _bin_and_blend(self, A, n, record, rect, tiles, depth_key, width, height, background, cs, tf, params,
-                       want_order, api) -> Frame:
+    def _bin_begin(self, A, n, record, rect, tiles, depth_key, width, height, background, cs, tf, params,
+                   want_order, api) -> dict:
         offsets = A.get("offsets", n + 1, torch.int64)
         kept_idx = A.get("kept_idx", n + 1, torch.int64)
         counts = A.get("counts", 2, torch.int64)
@@ -250,7 +257,24 @@ class Rasterizer:
         ws = A.get("ws_count", wsz, torch.uint8)
         self._run("vegs_bin_count", _p(tiles), n, _p(offsets), _p(kept_idx), _p(counts), _p(ws),
              ctypes.byref(ctypes.c_size_t(wsz)), s)
-        n_kept, n_inst = (int(x) for x in counts.tolist())  # the one host sync per view
+        host = torch.empty(2, dtype=torch.int64, pin_memory=True)
+        host.copy_(counts, non_blocking=True)
+        ev = torch.cuda.Event()
+        ev.record()
+        return dict(A=A, n=n, record=record, rect=rect, tiles=tiles, depth_key=depth_key, width=width,
+                    height=height, background=background, cs=cs, tf=tf, params=params, want_order=want_order,
+                    api=api, offsets=offsets, kept_idx=kept_idx, host=host, event=ev)
+
+    def forward_end(self, pend: dict) -> Frame:
+        """Second half: wait for the instance count (the one host sync per view), then sort
+        and composite on the current stream."""
+        A, n, record, rect, tiles, depth_key = (pend[k] for k in ("A", "n", "record", "rect", "tiles", "depth_key"))
+        width, height, background, cs, tf, params = (pend[k] for k in ("width", "height", "background", "cs", "tf",
+                                                                       "params"))
+        want_order, api, offsets, kept_idx = pend["want_order"], pend["api"], pend["offsets"], pend["kept_idx"]
+        s = _stream()
+        pend["event"].synchronize()
+        n_kept, n_inst = (int(x) for x in pend["host"].tolist())
         self.last_counts = (n_kept, n_inst)
         tiles_x = (width + TILE - 1) // TILE
         n_tiles = tiles_x * ((height + TILE - 1) // TILE)

@@ -163,6 +163,29 @@ class View:
     target: torch.Tensor  # (H, W, 3) float32 on the device
 
 
+class _Lane:
+    """One CUDA stream of the view pipeline with its own scratch (see Trainer)."""
+
+    def __init__(self, tr: "Trainer", stream):
+        from .device import LossKernel
+
+        self.stream = stream
+        self.rz = Rasterizer(tr.settings, 11 if tr.with_aux else 3, store_f64=False, pooled=True)
+        self.loss = LossKernel(tr.device)
+        self.loss_launches = 0
+        self.d_img = None
+        self.grads = None
+        self.dstats = None
+
+    def prepare(self, tr: "Trainer") -> None:
+        if self.grads is None or self.grads.numel() != tr.params.numel():
+            self.grads = torch.zeros_like(tr.params)
+        if tr.densify_stats is None:
+            self.dstats = None
+        elif self.dstats is None or self.dstats.numel() != tr.densify_stats.numel():
+            self.dstats = torch.zeros_like(tr.densify_stats)
+
+
 class Trainer:
     """Multi-view training step on device-resident float64 parameters.
 
@@ -170,10 +193,12 @@ class Trainer:
     GPUs; the gradient buffer is all-reduced once per step."""
 
     def __init__(self, gs: GaussianSet, config: TrainConfig, settings: RasterSettings = DEFAULT_SETTINGS,
-                 background=(1.0, 1.0, 1.0), l1_weight: float | None = None, group=None, with_aux: bool = False):
+                 background=(1.0, 1.0, 1.0), l1_weight: float | None = None, group=None, with_aux: bool = False,
+                 lanes: int = 2):
         self.device = require_cuda()
         self.n = len(gs)
         self.config = config
+        self.settings = settings
         self.background = tuple(float(x) for x in background)
         self.lam = float(config.lambda_ssim)
         self.w_l1 = (1.0 - self.lam) if l1_weight is None else float(l1_weight)
@@ -186,42 +211,83 @@ class Trainer:
         # with_aux: blend the 11 planes (rgb, depth, normal, attrs) and apply the normal /
         # smoothness regularisers, as the reference's loop does (train.py:476-479)
         self.with_aux = with_aux
-        self.rz = Rasterizer(settings, 11 if with_aux else 3, store_f64=False, pooled=True)
         self.group = group
         self.densify_stats = None  # (n, 5) float64 when densification is tracked
-        self._d_img = None
-        self._sums = None
+        # Views are pipelined over `lanes` CUDA streams, each with its own scratch pool,
+        # loss workspace and gradient buffer: one view's preprocess, count readback and
+        # sort overlap the previous view's compositing.  Lane 0 runs on the caller's stream.
+        self.lanes = [_Lane(self, torch.cuda.current_stream() if i == 0 else torch.cuda.Stream(self.device))
+                      for i in range(max(1, lanes))]
+        self.lanes[0].grads = self.grads
+        self.rz = self.lanes[0].rz
+
+    def set_timer(self, timer) -> None:
+        for lane in self.lanes:
+            lane.rz.timer = timer
+
+    @property
+    def launches(self) -> int:
+        return sum(lane.rz.launches + lane.loss_launches for lane in self.lanes)
 
     def gaussians(self) -> GaussianSet:
         return GaussianSet.unpack(self.params.cpu().numpy(), self.n)
 
-    def accumulate_view(self, view: View, scale: float, first: bool, sums: torch.Tensor) -> None:
-        fr = self.rz.forward(self.params, self.n, view.tf, view.camera, self.background)
+    def _loss_and_backward(self, lane, fr, view: View, scale: float, first: bool, sums: torch.Tensor) -> None:
         h, w = fr.height, fr.width
         img = fr.out_img.view(h, w, fr.n_ch)
-        if self._d_img is None or self._d_img.numel() != img.numel():
-            self._d_img = torch.empty_like(img)
-        l1_ssim_device(img, view.target, self.w_l1, self.lam, self._d_img, sums[:2])
+        if lane.d_img is None or lane.d_img.numel() != img.numel():
+            lane.d_img = torch.empty_like(img)
+        lane.loss(img, view.target, self.w_l1, self.lam, lane.d_img, sums[:2])
+        lane.loss_launches += 2
         if self.with_aux:
-            from .loss import _kernel
-
             cam = view.camera
             px_scale = 2.0 * math.tan(0.5 * cam.fov_y) / cam.height
-            _kernel().aux(img, fr.out_t.view(h, w), view.target, px_scale, self.config.normal_loss_weight,
-                          self.config.smooth_loss_weight, self._d_img, sums[2:5])
-        self.rz.backward(fr, self._d_img, None, self.grads, scale=scale, accumulate=not first,
-                         densify_stats=self.densify_stats)
+            lane.loss.aux(img, fr.out_t.view(h, w), view.target, px_scale, self.config.normal_loss_weight,
+                          self.config.smooth_loss_weight, lane.d_img, sums[2:5])
+            lane.loss_launches += 3
+        lane.rz.backward(fr, lane.d_img, None, lane.grads, scale=scale, accumulate=not first,
+                         densify_stats=lane.dstats)
 
     def step(self, views: list[View], total_views: int | None = None, iteration: int | None = None,
              scene_extent: float = 1.0) -> torch.Tensor:
         """One optimisation step over this rank's views; returns the mean loss over
-        this rank's views as a device scalar (no host sync)."""
+        this rank's views as a device scalar (no host sync besides the per-view counts)."""
+        main = torch.cuda.current_stream()
         total = total_views if total_views is not None else len(views)
-        sums = torch.zeros(len(views), 5, dtype=torch.float64, device=self.device)
-        if not views:
+        n_v = len(views)
+        sums = torch.zeros(n_v, 5, dtype=torch.float64, device=self.device)
+        lanes = self.lanes
+        for lane in lanes[1:]:
+            lane.prepare(self)
+            lane.stream.wait_stream(main)  # parameters updated, sums zeroed
+        lanes[0].grads = self.grads
+        lanes[0].dstats = self.densify_stats
+        pend: list = [None] * n_v
+        used = [False] * len(lanes)
+
+        def begin(i: int) -> None:
+            lane = lanes[i % len(lanes)]
+            with torch.cuda.stream(lane.stream):
+                pend[i] = lane.rz.forward_begin(self.params, self.n, views[i].tf, views[i].camera, self.background)
+
+        if n_v:
+            begin(0)
+        for i in range(n_v):
+            if i + 1 < n_v:
+                begin(i + 1)  # queue the next view's preprocess before waiting on this one's count
+            k = i % len(lanes)
+            lane = lanes[k]
+            with torch.cuda.stream(lane.stream):
+                fr = lane.rz.forward_end(pend[i])
+                pend[i] = None
+                self._loss_and_backward(lane, fr, views[i], 1.0 / total, not used[k], sums[i])
+            used[k] = True
+        if not used[0]:
             self.grads.zero_()
-        for i, view in enumerate(views):
-            self.accumulate_view(view, 1.0 / total, i == 0, sums[i])
+        for k, lane in enumerate(lanes[1:], start=1):
+            main.wait_stream(lane.stream)
+            if used[k]:
+                self.grads.add_(lane.grads)
         allreduce_gradients(self.grads, self.group)
         self.step_count += 1
         it = self.step_count if iteration is None else iteration
@@ -245,12 +311,23 @@ class Trainer:
         """Accumulate DensifyStats (per view, fused into the backward) from now on."""
         self.densify_stats = torch.zeros(self.n * 5, dtype=torch.float64, device=self.device) if on else None
 
+    def gather_densify_stats(self) -> torch.Tensor:
+        """Fold every lane's DensifyStats into ``densify_stats`` (n x 5) and return it."""
+        main = torch.cuda.current_stream()
+        for lane in self.lanes[1:]:
+            main.wait_stream(lane.stream)
+            if lane.dstats is not None and lane.dstats.numel() == self.densify_stats.numel():
+                self.densify_stats.add_(lane.dstats)
+                lane.dstats.zero_()
+        return self.densify_stats
+
     def densify_and_prune(self, scene_extent: float, rng: np.random.Generator, position_lr: float) -> int:
         """Device densify/prune of the resident set; the step's buffers are resized and
         the densification statistics reset.  With world_size > 1 the statistics are
         all-reduced first so every replica makes the same decision.  Returns the new n."""
         if self.densify_stats is None:
             raise RuntimeError("call track_densify() before training steps to collect statistics")
+        self.gather_densify_stats()
         allreduce_gradients(self.densify_stats, self.group)
         p, m, v, n_out = densify_device(self.params, self.m, self.v, self.n, self.densify_stats, self.config,
                                         scene_extent, rng, position_lr)

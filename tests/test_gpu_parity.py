@@ -410,7 +410,7 @@ def test_trainer_densify_tracks_stats_and_resizes():
     views = [View(c, dtf, t) for c, t in zip(cams, targets)]
     for _ in range(3):
         tr.step(views)
-    st = tr.densify_stats.view(-1, 5).cpu().numpy()
+    st = tr.gather_densify_stats().view(-1, 5).cpu().numpy()
     assert st[:, 4].max() == 6.0 and (st[:, 0] > 0).any()  # 3 steps x 2 views
     n_before = tr.n
     n_after = tr.densify_and_prune(3.0, np.random.default_rng(0), 1e-4)

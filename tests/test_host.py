@@ -41,7 +41,7 @@ def test_struct_layouts_match_header():
 
 
 def test_loss_workspace_query_runs_without_a_gpu():
-    b3 = _lib.size_query("vegs_loss_l1_ssim", None, None, 64, 64, 0.8, 0.2, None, None, tail=(None,))
+    b3 = _lib.size_query("vegs_loss_l1_ssim", None, None, 64, 64, 3, 0.8, 0.2, None, None, tail=(None,))
     assert b3 == 4 * 9 * 54 * 54
 
 
