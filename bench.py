@@ -239,24 +239,26 @@ def run_b200(args) -> None:
     loss_val = float(loss.item())
     trainer.check_finite()
 
-    # ---- forward render throughput over the same views
-    rz = trainer.rz
+    # ---- forward render throughput over the same views (two-lane render pipeline)
+    from paper_2504_13339_b200.device import RenderPipeline
+
+    pipe = RenderPipeline()
+    items = [(v.camera, dtf) for v in views]
     for _ in range(2):
-        for v in views:
-            rz.forward(trainer.params, trainer.n, dtf, v.camera)
+        pipe.render(trainer.params, trainer.n, items)
     barrier()
     torch.cuda.synchronize()
     r0, r1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     r0.record()
     for _ in range(args.render_frames):
-        for v in views:
-            rz.forward(trainer.params, trainer.n, dtf, v.camera)
+        pipe.render(trainer.params, trainer.n, items)
     r1.record()
     torch.cuda.synchronize()
     barrier()
     rms = max_over_ranks(r0.elapsed_time(r1))
     px = args.render_frames * VIEWS_PER_STEP * 1024 * 1024
     render_mpx_s = px / (rms / 1000.0) / 1e6
+    del pipe
 
     # ---- end to end through the public API with host buffers
     h2d = sum(t.numel() * t.element_size() for t in host_targets)
@@ -336,19 +338,17 @@ def run_sweep(args, dev, rank, world) -> dict:
     cams = scenes.orbit_cameras(n_frames, 5, 1920, 1080)
     mine = [f for f in range(n_frames) if f % world == rank]
     tfs = {f: [DeviceTF(scenes.random_tf(1000 + 8 * f + k), dev) for k in range(8)] for f in mine}
-    rz = Rasterizer(pooled=True)
-    for tf in tfs[mine[0]][:2]:
-        rz.forward(params, len(gs), tf, cams[mine[0]])
+    from paper_2504_13339_b200.device import RenderPipeline
+
+    pipe = RenderPipeline()
+    items = [(cams[f], tf) for f in mine for tf in tfs[f]]
+    pipe.render(params, len(gs), items[:2])
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
-    inst = 0
-    for f in mine:
-        for tf in tfs[f]:
-            fr = rz.forward(params, len(gs), tf, cams[f])
-            inst += fr.n_inst
+    inst = pipe.render(params, len(gs), items)
     e1.record()
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1)

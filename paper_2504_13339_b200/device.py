@@ -392,3 +392,47 @@ def adam_step_device(params, grads, m, v, n: int, lrs: torch.Tensor, grad_scale:
     b1, b2 = 0.9, 0.999
     call("vegs_adam_step", _p(params), _p(grads), _p(m), _p(v), n, _p(lrs), float(grad_scale),
          1.0 - b1 ** step, 1.0 - b2 ** step, _p(nonfinite), _stream())
+
+
+class RenderPipeline:
+    """Forward renders of many (camera, TF) pairs pipelined over CUDA streams: the next
+    render's preprocess and instance count are queued before waiting on the current one's
+    count, so the small per-view kernels overlap the previous view's compositing.
+    Output frames are only valid until the lane that produced them is reused."""
+
+    def __init__(self, settings: RasterSettings = DEFAULT_SETTINGS, n_channels: int = 3, lanes: int = 2):
+        dev = require_cuda()
+        main = torch.cuda.current_stream()
+        self.lanes = [(main if i == 0 else torch.cuda.Stream(dev), Rasterizer(settings, n_channels, pooled=True))
+                      for i in range(max(1, lanes))]
+
+    def render(self, params: torch.Tensor, n: int, items, background=(1.0, 1.0, 1.0), on_frame=None) -> int:
+        """items: list of (camera, DeviceTF).  on_frame(i, frame) is called (on the frame's
+        stream) right after each composite.  Returns the total instance count."""
+        main = torch.cuda.current_stream()
+        for s, _ in self.lanes[1:]:
+            s.wait_stream(main)
+        L = len(self.lanes)
+        pend = [None] * len(items)
+
+        def begin(i):
+            s, rz = self.lanes[i % L]
+            with torch.cuda.stream(s):
+                pend[i] = rz.forward_begin(params, n, items[i][1], items[i][0], background)
+
+        total = 0
+        if items:
+            begin(0)
+        for i in range(len(items)):
+            if i + 1 < len(items):
+                begin(i + 1)
+            s, rz = self.lanes[i % L]
+            with torch.cuda.stream(s):
+                fr = rz.forward_end(pend[i])
+                pend[i] = None
+                total += fr.n_inst
+                if on_frame is not None:
+                    on_frame(i, fr)
+        for s, _ in self.lanes[1:]:
+            main.wait_stream(s)
+        return total
