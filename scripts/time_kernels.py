@@ -1,0 +1,46 @@
+"""Quick timing of the compositing kernels on one config-2 view (CUDA events, single
+stream): python scripts/time_kernels.py [reps]"""
+import sys
+from pathlib import Path
+
+import torch
+
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+
+from paper_2504_13339_b200 import scenes  # noqa: E402
+from paper_2504_13339_b200.device import DeviceTF, Rasterizer  # noqa: E402
+
+
+def main():
+    reps = int(sys.argv[1]) if len(sys.argv) > 1 else 10
+    gs, truth, tf, cams = scenes.config_scene("c2")
+    dtf = DeviceTF(tf)
+    rz = Rasterizer()
+    params = torch.from_numpy(gs.pack()).cuda()
+    grads = torch.zeros_like(params)
+    times = {"vegs_composite_forward": [], "vegs_composite_backward": []}
+
+    class T:
+        def mark(self, name, begin, rz=None):
+            if name in times:
+                ev = torch.cuda.Event(enable_timing=True)
+                ev.record()
+                if begin:
+                    self.s = ev
+                else:
+                    times[name].append((self.s, ev))
+
+    d_img = torch.rand(1024, 1024, 3, device="cuda") - 0.5
+    for r in range(reps + 2):
+        rz.timer = T() if r >= 2 else None
+        for cam in cams[:4]:
+            fr = rz.forward(params, len(gs), dtf, cam)
+            rz.backward(fr, d_img, None, grads)
+    torch.cuda.synchronize()
+    for k, v in times.items():
+        ms = [a.elapsed_time(b) for a, b in v]
+        print(f"{k}: {sum(ms) / len(ms):.3f} ms avg over {len(ms)}")
+
+
+if __name__ == "__main__":
+    main()
