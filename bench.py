@@ -60,16 +60,19 @@ def parse():
     ap.add_argument("--cpu-budget-s", type=float, default=60.0)
     ap.add_argument("--no-sweep", action="store_true", help="skip the config-3 TF-sweep render measurement")
     ap.add_argument("--sweep-frames", type=int, default=2)
+    ap.add_argument("--backend", choices=("nccl", "gloo"), default="nccl",
+                    help="gradient all-reduce backend for N>1 (gloo: host-side plumbing check only)")
     return ap.parse_args()
 
 
-def config_block(world: int) -> dict:
+def config_block(world: int, backend: str = "nccl") -> dict:
     return {"workload": "c2: 1M Gaussians (seed 0) fit to renders of a 1M-Gaussian 64-blob set (seed 1); "
                         "16 views/step at 1024x1024, 256-knot TF; step = render + L1/SSIM + backward "
                         "+ all-reduce + Adam",
             "n_gaussians": 1_000_000, "views_per_step": VIEWS_PER_STEP, "width": 1024, "height": 1024,
             "loss": "0.8*L1 + 0.2*(1-SSIM) (reference (1-lambda) weighting)",
-            "parallelism": f"view-sharded dp{world}", "l2": "inputs larger than L2 (no flush needed)"}
+            "parallelism": f"view-sharded dp{world}" + ("" if world == 1 or backend == "nccl" else f" ({backend})"),
+            "l2": "inputs larger than L2 (no flush needed)"}
 
 
 def peaks() -> tuple[float, str]:
@@ -173,10 +176,11 @@ def run_b200(args) -> None:
 
     from paper_2504_13339_b200 import scenes
     from paper_2504_13339_b200.device import DeviceTF, Rasterizer
-    from paper_2504_13339_b200.parallel import init_from_env, shard_views
+    from paper_2504_13339_b200.parallel import init_from_env, local_device, shard_views
     from paper_2504_13339_b200.train import TrainConfig, Trainer, View
 
-    rank, world, local = init_from_env("nccl")
+    rank, world, local = init_from_env(args.backend)
+    local = local_device(local, args.backend)
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     learned, truth, tf, cams = scenes.config_scene(WORKLOAD)
@@ -314,7 +318,7 @@ def run_b200(args) -> None:
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": max(args.warmup, 3), "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f32+f64", "data": "synthetic (seeded, scenes.py)",
-            "config": config_block(world), "e2e": e2e, "render_mpx_s": render_mpx_s, "loss": loss_val,
+            "config": config_block(world, args.backend), "e2e": e2e, "render_mpx_s": render_mpx_s, "loss": loss_val,
             "gpu_launches": int(launches), "roofline": roof, "kernels": kernels, "render_sweep_c3": sweep,
             "cpu_baseline": cpu,
             "clocks": clk}

@@ -46,3 +46,14 @@ def init_from_env(backend: str = "nccl") -> tuple[int, int, int]:
         else:
             dist.init_process_group(backend)
     return rank, world, local
+
+
+def local_device(local: int, backend: str = "nccl") -> int:
+    """CUDA ordinal for this rank.  NCCL needs one GPU per rank; the gloo plumbing check
+    (host-side collectives, no kernel waits on another rank) may fold ranks onto fewer GPUs."""
+    n = torch.cuda.device_count()
+    if local < n:
+        return local
+    if backend == "nccl":
+        raise RuntimeError(f"local rank {local} but only {n} GPU(s): NCCL needs one GPU per rank")
+    return local % n

@@ -22,7 +22,7 @@ import torch
 
 from .camera import Camera
 from .constants import DEFAULT_SETTINGS, RasterSettings
-from .device import DeviceTF, Frame, Rasterizer, require_cuda
+from .device import DeviceTF, Frame, Rasterizer, rec_stride, require_cuda
 from .images import ImageBuffer
 from .model import BETA_MAX, FLOATS_PER_GAUSSIAN, GaussianSet, PARAM_CLASSES
 from .transfer import TransferFunction
@@ -131,8 +131,8 @@ class BlendState:
 
     def _inst_record(self, lo, hi):
         fr = self._frame
-        rs = fr.record.numel() // max(fr.n, 1)
-        rec = fr.record.view(-1, rs)[fr.sorted_gauss[:fr.n_inst].long()]
+        rs = rec_stride(fr.n_ch)
+        rec = fr.record[: fr.n * rs].view(fr.n, rs)[fr.sorted_gauss[:fr.n_inst].long()]
         return _np(rec[:, lo:hi])
 
     @property
@@ -158,7 +158,7 @@ class BlendState:
     @property
     def inst_rect(self):
         fr = self._frame
-        return self._get("rect", lambda: _np(fr.rect.view(-1, 4)[fr.sorted_gauss[:fr.n_inst].long()]))
+        return self._get("rect", lambda: _np(fr.rect[: 4 * fr.n].view(fr.n, 4)[fr.sorted_gauss[:fr.n_inst].long()]))
 
     @property
     def out_t(self):
@@ -242,18 +242,21 @@ def _upload_params(gs: GaussianSet, device) -> torch.Tensor:
 
 def _splat_views(fr: Frame, gs_len: int, with_aux: bool):
     kept = _np(torch.nonzero(fr.tiles[:gs_len] != 0).flatten()).astype(np.int64)
-    a = {k: _np(v) for k, v in fr.api.items()}
-    aux = a["aux"].reshape(gs_len, 24)
     n = gs_len
-    sh = ShadeResult(color=a["color"].reshape(n, 3), alpha_base=a["alpha_base"], visible=a["visible"].astype(bool),
+    # pool buffers hold at least one element, so cut every table column to n rows
+    a = {k: _np(v) for k, v in fr.api.items()}
+    cut = {"aux": 24, "color": 3, "mean2d": 2, "conic": 3}
+    a = {k: (v[: n * cut[k]].reshape(n, cut[k]) if k in cut else v[:n]) for k, v in a.items()}
+    aux = a["aux"]
+    sh = ShadeResult(color=a["color"], alpha_base=a["alpha_base"], visible=a["visible"].astype(bool),
                      v=aux[:, 0].copy(), w=aux[:, 1].copy(), opacity=aux[:, 2].copy(), cmap=aux[:, 3:6].copy(),
                      light=aux[:, 6:9].copy(), light_dist=aux[:, 9].copy(), n_hat=aux[:, 10:13].copy(),
                      n_norm=aux[:, 13].copy(), ndotl=aux[:, 14].copy(), ka=aux[:, 15].copy(), kd=aux[:, 16].copy(),
                      ks=aux[:, 17].copy(), beta=aux[:, 18].copy(), spec_pow=aux[:, 19].copy())
     vis_idx = np.flatnonzero(sh.visible)
     in_view = np.isin(vis_idx, kept)
-    rect = _np(fr.rect.view(-1, 4)[:n])[kept].astype(np.int32)
-    proj = ProjectResult(in_view=in_view, mean2d=a["mean2d"].reshape(n, 2)[kept], conic=a["conic"].reshape(n, 3)[kept],
+    rect = _np(fr.rect[: 4 * n].view(n, 4))[kept].astype(np.int32)
+    proj = ProjectResult(in_view=in_view, mean2d=a["mean2d"][kept], conic=a["conic"][kept],
                          cov2d=aux[kept, 20:23].copy(), depth=a["depth"][kept], radius=a["radius"][kept], rect=rect)
     ch = np.zeros((len(kept), N_AUX_CHANNELS if with_aux else 3))
     ch[:, :3] = sh.color[kept]

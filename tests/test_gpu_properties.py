@@ -1,0 +1,153 @@
+"""Property tests of the CUDA rasteriser, after the reference's own (pkg/tests/
+test_rasterize.py:98-206): permutation invariance, colour-map independence of alpha,
+determinism, zero / inert / occluded gradients, f32 vs f64 agreement, and edge cases
+(empty set, everything culled, partial tiles, tiny images)."""
+
+import math
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("needs CUDA", allow_module_level=True)
+
+from paper_2504_13339_b200 import raster as R  # noqa: E402
+from paper_2504_13339_b200 import scenes  # noqa: E402
+from paper_2504_13339_b200.camera import Camera  # noqa: E402
+from paper_2504_13339_b200.model import GaussianSet, logit  # noqa: E402
+from paper_2504_13339_b200.transfer import ColorMap, OpacityMap, TransferFunction  # noqa: E402
+
+
+def small_scene(seed, n=400, res=48):
+    gs = scenes.random_gaussians(n, seed=seed)
+    gs.log_scale[:] += 1.0  # splats a few pixels wide at this resolution
+    tf = scenes.random_tf(seed + 100, 3)
+    cam = scenes.orbit_cameras(1, seed + 200, res, res)[0]
+    return gs, tf, cam
+
+
+def test_permuting_input_order_changes_nothing():
+    gs, tf, cam = small_scene(1)
+    a = R.render(gs, tf, cam, (0.3, 0.4, 0.5), dtype=np.float32)
+    perm = np.random.default_rng(0).permutation(len(gs))
+    b = R.render(gs.select(perm), tf, cam, (0.3, 0.4, 0.5), dtype=np.float32)
+    assert np.array_equal(a.rgb, b.rgb) and np.array_equal(a.alpha, b.alpha)
+
+
+def test_colour_map_swap_keeps_alpha_bitwise():
+    gs, tf, cam = small_scene(2)
+    planes = []
+    for seed in range(4):
+        rng = np.random.default_rng(seed)
+        ts = np.concatenate([[0.0], np.sort(rng.uniform(0, 1, 5)), [1.0]])
+        cm = ColorMap(tuple((float(t),) + tuple(rng.uniform(0, 1, 3)) for t in ts))
+        planes.append(R.render(gs, TransferFunction(color=cm, opacity=tf.opacity), cam, dtype=np.float32).alpha)
+    assert all(np.array_equal(planes[0], p) for p in planes[1:])
+
+
+def test_render_and_backward_deterministic():
+    gs, tf, cam = small_scene(3)
+    d = np.random.default_rng(1).uniform(-1, 1, size=(cam.height, cam.width, 3))
+    outs = []
+    for _ in range(2):
+        img, st = R.render_with_state(gs, tf, cam, dtype=np.float32)
+        outs.append((img, R.rasterize_backward(st, R.ImageGradients(rgb=d))))
+    assert np.array_equal(outs[0][0].rgb, outs[1][0].rgb)
+    for k, v in outs[0][1].arrays().items():
+        assert np.array_equal(v, getattr(outs[1][1], k)), k
+
+
+def test_zero_image_gradient_gives_zero_parameter_gradients():
+    gs, tf, cam = small_scene(4)
+    _, st = R.render_with_state(gs, tf, cam, with_aux=True, dtype=np.float32)
+    g = R.rasterize_backward(st, R.ImageGradients(rgb=np.zeros((cam.height, cam.width, 3))))
+    for k, v in g.arrays().items():
+        assert np.all(v == 0.0), k
+
+
+def test_subthreshold_splat_is_inert():
+    data = R.SplatData(mean2d=np.array([[16.0, 16.0], [10.0, 12.0]]),
+                       conic=np.array([[0.5, 0.0, 0.5], [0.3, 0.05, 0.4]]),
+                       alpha_base=np.array([0.6, 0.5 / 255.0]), depth=np.array([1.0, 0.5]),
+                       rect=np.array([[0, 32, 0, 32], [0, 32, 0, 32]], dtype=np.int32),
+                       channels=np.array([[0.2, 0.4, 0.6], [1.0, 1.0, 1.0]]))
+    with_low, _ = R.rasterize_forward(data, 32, 32, (0.1, 0.1, 0.1), dtype=np.float32)
+    only = R.SplatData(**{k: getattr(data, k)[:1] for k in ("mean2d", "conic", "alpha_base", "depth", "rect",
+                                                            "channels")})
+    without, _ = R.rasterize_forward(only, 32, 32, (0.1, 0.1, 0.1), dtype=np.float32)
+    assert np.array_equal(with_low.rgb, without.rgb)
+
+
+def test_fully_occluded_splat_gets_zero_gradient():
+    n_wall = 10
+    pos = [[0.0, 0.0, 0.5 + 0.05 * i] for i in range(n_wall)] + [[0.0, 0.0, -2.0]]
+    n = n_wall + 1
+    gs = GaussianSet(position=np.array(pos), log_scale=np.full((n, 3), math.log(4.0)),
+                     rotation=np.tile([1.0, 0.0, 0.0, 0.0], (n, 1)), raw_value=np.full(n, float(logit(0.5))),
+                     raw_weight=np.full(n, float(logit(0.97))), normal=np.tile([0.0, 0.0, 1.0], (n, 1)),
+                     raw_ka=np.zeros(n), raw_kd=np.zeros(n), raw_ks=np.zeros(n), raw_beta=np.full(n, math.log(8.0)))
+    tf = TransferFunction(color=ColorMap(((0.0, 0.2, 0.3, 0.4), (1.0, 0.9, 0.8, 0.1))),
+                          opacity=OpacityMap(((0.0, 0.95), (1.0, 0.95))))
+    cam = Camera(position=(0.0, 0.0, 4.0), target=(0.0, 0.0, 0.0), width=32, height=32, fov_y=math.radians(45.0))
+    img, st = R.render_with_state(gs, tf, cam, (0.0, 0.0, 0.0), with_aux=True, dtype=np.float32)
+    wall = R.render(gs.select(np.arange(n_wall)), tf, cam, (0.0, 0.0, 0.0), with_aux=True, dtype=np.float32)
+    assert np.array_equal(img.rgb, wall.rgb)
+    g = R.rasterize_backward(st, R.ImageGradients(rgb=np.ones((32, 32, 3))))
+    for k, v in g.arrays().items():
+        assert np.all(v[n_wall] == 0.0), k
+    assert np.abs(g.raw_value[n_wall - 3:n_wall]).max() > 0.0
+
+
+def test_rgb_only_render_has_no_aux_planes():
+    gs, tf, cam = small_scene(5)
+    img = R.render(gs, tf, cam, with_aux=False)
+    assert img.depth is None and img.normal is None and img.attrs is None
+
+
+def test_float32_close_to_float64():
+    gs, tf, cam = small_scene(6)
+    a = R.render(gs, tf, cam, dtype=np.float64)
+    b = R.render(gs, tf, cam, dtype=np.float32)
+    assert np.abs(a.rgb - b.rgb).max() < 1e-4
+
+
+@pytest.mark.parametrize("dtype", [np.float32, np.float64])
+def test_empty_set_is_background(dtype):
+    gs = scenes.random_gaussians(1, seed=0).select(np.arange(0))
+    tf = scenes.random_tf(1, 2)
+    cam = scenes.orbit_cameras(1, 0, 40, 24)[0]
+    img, st = R.render_with_state(gs, tf, cam, (0.25, 0.5, 0.75), dtype=dtype)
+    assert np.allclose(img.rgb, [0.25, 0.5, 0.75]) and np.all(img.alpha == 0.0)
+    assert len(st.blend.order) == 0 and np.all(st.blend.out_last == -1)
+    g = R.rasterize_backward(st, R.ImageGradients(rgb=np.ones((24, 40, 3))))
+    assert g.position.shape == (0, 3)
+
+
+def test_everything_culled():
+    gs = scenes.random_gaussians(200, seed=3)
+    gs.raw_weight[:] = -20.0  # alpha_base far below 1/255: every splat culled before projection
+    tf = scenes.random_tf(3, 2)
+    cam = scenes.orbit_cameras(1, 4, 33, 17)[0]
+    img, st = R.render_with_state(gs, tf, cam, (1.0, 1.0, 1.0), dtype=np.float32)
+    assert len(st.kept) == 0 and np.all(img.rgb == 1.0)
+    g = R.rasterize_backward(st, R.ImageGradients(rgb=np.ones((17, 33, 3))))
+    assert all(np.all(v == 0) for v in g.arrays().values()) and not g.visible.any()
+
+
+@pytest.mark.parametrize("wh", [(1, 1), (5, 3), (17, 33), (250, 130)])
+def test_partial_tiles_match_oracle(wh):
+    from oracle import vegs_oracle as O
+    from paper_2504_13339_b200.constants import DEFAULT_SETTINGS as S
+
+    gs = scenes.random_gaussians(3000, seed=7)
+    tf = scenes.random_tf(7, 4)
+    cam = scenes.orbit_cameras(1, 8, wh[0], wh[1])[0]
+    img, st = R.render_with_state(gs, tf, cam, (0.5, 0.5, 0.5), S, False, np.float32)
+    img_o, st_o = O.render_with_state(gs, tf, cam, (0.5, 0.5, 0.5), S, False, np.float32)
+    assert np.array_equal(st.blend.order, st_o["order"])
+    assert np.array_equal(st.blend.out_last, st_o["out_last"])
+    assert np.array_equal(st.blend.n_contrib, st_o["n_contrib"])
+    assert np.abs(img.rgb - img_o["rgb"]).max() < 1e-5
