@@ -145,22 +145,22 @@ int vegs_composite_forward(const int32_t *tile_start, const int32_t *tile_end,
                            void *out_t, int32_t *out_last, int32_t *n_contrib, void *stream);
 
 /* Backward tile blend.  d_img H x W x C, d_alpha H x W (storage type).  Writes per-
- * instance rows [g_mx, g_my, g_ca, g_cb, g_cc, g_alpha, g_ch..., stamp] (row stride
- * rec_stride) at the instance's duplicate-order index inst_pid[s].  Rows of instances no
- * pixel blended are not written; written rows carry `stamp` (64 bits in the padding) and
- * vegs_preprocess_backward ignores rows without it, so use a fresh stamp per call. */
+ * instance rows [g_mx, g_my, g_ca, g_cb, g_cc, g_alpha, g_ch..., pad] (row stride
+ * rec_stride) at the instance's duplicate-order index p = inst_pid[s] and sets bit p of
+ * inst_visited (ceil(n_inst / 32) words, zeroed by this call).  Rows of instances no
+ * pixel blended are not written; vegs_preprocess_backward reads only visited rows. */
 int vegs_composite_backward(const int32_t *tile_start, const int32_t *tile_end,
                             const uint32_t *sorted_gauss, const uint32_t *inst_pid,
                             const void *record, const int32_t *rect, int32_t n_channels,
                             int32_t store_f64, const double *bg, int32_t width, int32_t height,
                             double alpha_clamp, const void *out_t, const int32_t *out_last,
-                            const void *d_img, const void *d_alpha, void *inst_rows, uint64_t stamp,
-                            void *stream);
+                            const void *d_img, const void *d_alpha, void *inst_rows,
+                            uint32_t *inst_visited, int64_t n_inst, void *stream);
 
 /* Per-Gaussian: float64 reduction of its instance rows (duplicate order == np.add.at
  * order), then projection and shading backward.  grads: flat float64 class-major
  * buffer (19 n); grads = accumulate ? grads + scale * g : scale * g.  viewspace_norm /
- * visible may be NULL.  Only rows carrying row_stamp are summed.  densify_stats (n x 5,
+ * visible may be NULL.  Only rows whose inst_visited bit is set are summed.  densify_stats (n x 5,
  * may be NULL) accumulates DensifyStats for the kept splats.  ws holds the per-Gaussian
  * sums (n x (6 + C) float64). */
 int vegs_preprocess_backward(const double *params, int64_t n, const VegsCamera *cam,
@@ -168,8 +168,8 @@ int vegs_preprocess_backward(const double *params, int64_t n, const VegsCamera *
                              int32_t store_f64, const uint32_t *tiles, const int64_t *offsets,
                              const void *inst_rows, double scale, int32_t accumulate,
                              double *grads, double *viewspace_norm, uint8_t *visible,
-                             double *densify_stats, uint64_t row_stamp, void *ws, size_t *ws_bytes,
-                             void *stream);
+                             double *densify_stats, const uint32_t *inst_visited, void *ws,
+                             size_t *ws_bytes, void *stream);
 
 /* ---- drop-in raw kernels (reference argument lists) -------------------------------- */
 int vegs_blend_forward(const int64_t *tile_start, const int64_t *tile_end, int64_t n_tiles,

@@ -60,9 +60,9 @@ _SIGS = {
     "vegs_composite_forward": [P, P, P, P, P, c_int32, c_int32, P, c_int32, c_int32, c_double, c_double,
                                P, P, P, P, P],
     "vegs_composite_backward": [P, P, P, P, P, P, c_int32, c_int32, P, c_int32, c_int32, c_double, P, P,
-                                P, P, P, c_uint64, P],
+                                P, P, P, P, c_int64, P],
     "vegs_preprocess_backward": [P, c_int64, POINTER(VegsCamera), POINTER(VegsTF), POINTER(VegsSettings),
-                                 c_int32, c_int32, P, P, P, c_double, c_int32, P, P, P, P, c_uint64, P,
+                                 c_int32, c_int32, P, P, P, c_double, c_int32, P, P, P, P, P, P,
                                  POINTER(c_size_t), P],
     "vegs_densify_count": [P, c_int64, P, POINTER(VegsDensify), P, P, P, POINTER(c_size_t), P],
     "vegs_densify_apply": [P, P, P, c_int64, P, POINTER(VegsDensify), P, P, P, c_int64, P, P, P, P],
@@ -76,14 +76,6 @@ _SIGS = {
 }
 
 _lib = None
-_stamp = 0
-
-
-def next_stamp() -> int:
-    """Fresh 64-bit tag for backward row buffers (see vegs_composite_backward)."""
-    global _stamp
-    _stamp += 1
-    return (_stamp * 0x9E3779B97F4A7C15 + 1) & 0xFFFFFFFFFFFFFFFF
 
 
 class VegsError(RuntimeError):

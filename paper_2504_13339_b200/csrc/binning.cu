@@ -10,8 +10,10 @@
 // depths keep kept-index order (step 1 is stable on Gaussian index), and one splat never
 // has two instances in a tile.  Sorting only the tile id (2 onesweep passes on 16-bit
 // keys) instead of a (tile, depth-rank) key saves half the passes and a third of the
-// bytes per pass.  Instance payloads are the duplicate-order index p (rows of one
-// Gaussian are contiguous in p, which the deterministic backward reduction relies on).
+// bytes per pass.  The sort payload is the splat id itself; each instance's
+// duplicate-order index p (rows of one Gaussian are contiguous in p, which the
+// deterministic backward reduction relies on) is recomputed afterwards from the splat's
+// tile rectangle, so no per-instance indirection array is gathered.
 
 #include <cub/cub.cuh>
 
@@ -50,56 +52,72 @@ __global__ void iota_kernel(uint32_t *out, int64_t n) {
     if (i < n) out[i] = (uint32_t)i;
 }
 
-// depth rank of each kept splat + its tile count in depth order
-__global__ void rank_kernel(const uint32_t *sorted_ids, const uint32_t *tiles, int64_t n_kept, uint32_t *rank,
-                            uint32_t *count_d) {
+// tile count of each kept splat in depth order (the scan input for the depth-order offsets)
+__global__ void depth_counts_kernel(const uint32_t *sorted_ids, const uint32_t *tiles, int64_t n_kept,
+                                    uint32_t *count_d) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i > n_kept) return;
-    if (i == n_kept) {
-        count_d[i] = 0u;
-        return;
-    }
-    const uint32_t g = sorted_ids[i];
-    rank[g] = (uint32_t)i;
-    count_d[i] = tiles[g];
+    count_d[i] = i == n_kept ? 0u : tiles[sorted_ids[i]];
 }
 
-// One warp per Gaussian: lanes stride over the splat's tiles (row-major, pipeline.py:181-187),
-// writing tile keys at depth-order positions and duplicate-order payloads.
+struct SplatSpan {  // the splat's tile rectangle (pipeline.py:174-180)
+    int x0, y0, nx;
+};
+__device__ __forceinline__ SplatSpan splat_span(int4 r) {
+    SplatSpan sp;
+    sp.x0 = r.x / kTile;
+    sp.y0 = r.z / kTile;
+    sp.nx = (r.y - 1) / kTile - sp.x0 + 1;
+    return sp;
+}
+
+// Instances in depth order: thread i loads the i-th kept splat (coalesced), then the warp
+// walks its 32 splats one by one with the lanes striding over each splat's tiles
+// (row-major, pipeline.py:181-187), so key and value stores are coalesced runs.
 template <typename TKey>
-__global__ void duplicate_kernel(const uint32_t *tiles, const int32_t *rect, const int64_t *offsets,
-                                 const uint32_t *rank, const uint32_t *offs_d, int64_t n, int tiles_x, TKey *keys,
-                                 uint32_t *vals, uint32_t *inst_gauss) {
-    const int64_t g = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+__global__ void duplicate_kernel(const uint32_t *sorted_ids, const uint32_t *tiles, const int4 *rect,
+                                 const uint32_t *offs_d, int64_t n_kept, int tiles_x, TKey *keys, uint32_t *vals) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int lane = threadIdx.x & 31;
-    if (g >= n) return;
-    const uint32_t cnt = tiles[g];
-    if (cnt == 0) return;
-    const int x0 = rect[4 * g] / kTile, x1 = (rect[4 * g + 1] - 1) / kTile;
-    const int y0 = rect[4 * g + 2] / kTile;
-    const int nx = x1 - x0 + 1;
-    const int64_t base_p = offsets[g];
-    const int64_t base_d = offs_d[rank[g]];
-    for (uint32_t j = lane; j < cnt; j += 32) {
-        const int dy = (int)(j / nx), dx = (int)(j - dy * nx);
-        keys[base_d + j] = (TKey)((y0 + dy) * tiles_x + (x0 + dx));
-        vals[base_d + j] = (uint32_t)(base_p + j);
-        inst_gauss[base_p + j] = (uint32_t)g;
+    uint32_t g = 0, cnt = 0, base = 0;
+    SplatSpan sp{0, 0, 1};
+    if (i < n_kept) {
+        g = sorted_ids[i];
+        cnt = tiles[g];
+        base = offs_d[i];
+        sp = splat_span(__ldg(rect + g));
+    }
+    for (int k = 0; k < 32; ++k) {
+        const uint32_t ck = __shfl_sync(0xffffffffu, cnt, k);
+        if (ck == 0) continue;
+        const uint32_t bk = __shfl_sync(0xffffffffu, base, k), gk = __shfl_sync(0xffffffffu, g, k);
+        const int x0 = __shfl_sync(0xffffffffu, sp.x0, k), y0 = __shfl_sync(0xffffffffu, sp.y0, k);
+        const int nx = __shfl_sync(0xffffffffu, sp.nx, k);
+        for (uint32_t j = lane; j < ck; j += 32) {
+            const int dy = (int)(j / (uint32_t)nx), dx = (int)j - dy * nx;
+            keys[bk + j] = (TKey)((y0 + dy) * tiles_x + (x0 + dx));
+            vals[bk + j] = gk;
+        }
     }
 }
 
-// For each sorted instance: Gaussian id, optional kept index (`order`), and the
-// searchsorted tile ranges (empty tiles get start == end == insertion point).
+// For each sorted instance: its duplicate-order index p = offsets[g] + (row-major index of
+// the tile inside the splat's tile rectangle), optional kept index (`order`), and the
+// searchsorted tile ranges (empty tiles get start == end == insertion point).  The
+// per-splat gathers hit arrays of n entries (L2-resident).
 template <typename TKey>
-__global__ void finalize_kernel(const TKey *keys, const uint32_t *vals, const uint32_t *inst_gauss,
-                                const int64_t *kept_idx, int64_t n_inst, int n_tiles, uint32_t *sorted_gauss,
-                                int64_t *order, int32_t *tile_start, int32_t *tile_end) {
+__global__ void finalize_kernel(const TKey *keys, const uint32_t *sorted_gauss, const int4 *rect,
+                                const int64_t *offsets, const int64_t *kept_idx, int64_t n_inst, int n_tiles,
+                                int tiles_x, uint32_t *inst_pid, int64_t *order, int32_t *tile_start,
+                                int32_t *tile_end) {
     const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (s >= n_inst) return;
-    const uint32_t gid = inst_gauss[vals[s]];
-    sorted_gauss[s] = gid;
-    if (order) order[s] = kept_idx[gid];
+    const uint32_t gid = sorted_gauss[s];
     const int tile = (int)keys[s];
+    const SplatSpan sp = splat_span(__ldg(rect + gid));
+    const int ty = tile / tiles_x, tx = tile - ty * tiles_x;
+    inst_pid[s] = (uint32_t)(__ldg(offsets + gid) + (ty - sp.y0) * sp.nx + (tx - sp.x0));
+    if (order) order[s] = kept_idx[gid];
     const int prev = s > 0 ? (int)keys[s - 1] : -1;
     if (tile != prev) {
         for (int t = prev + 1; t <= tile; ++t) tile_start[t] = (int32_t)s;
@@ -168,7 +186,7 @@ static int bin_sort_impl(const uint32_t *tiles, const uint64_t *depth_key, const
     size_t t_max = t_depth > t_inst ? t_depth : t_inst;
     t_max = t_max > t_scan ? t_max : t_scan;
     const size_t b_tmp = align_up(t_max);
-    const size_t need = 2 * b_dk + 5 * b_id + 2 * b_k + 2 * b_v + b_tmp;
+    const size_t need = 2 * b_dk + 4 * b_id + 2 * b_k + b_v + b_tmp;
     if (!ws) {
         *ws_bytes = need;
         return VEGS_OK;
@@ -179,13 +197,11 @@ static int bin_sort_impl(const uint32_t *tiles, const uint64_t *depth_key, const
     uint64_t *dk1 = (uint64_t *)w; w += b_dk;
     uint32_t *id0 = (uint32_t *)w; w += b_id;
     uint32_t *id1 = (uint32_t *)w; w += b_id;
-    uint32_t *rank = (uint32_t *)w; w += b_id;
     uint32_t *count_d = (uint32_t *)w; w += b_id;
     uint32_t *offs_d = (uint32_t *)w; w += b_id;
     TKey *k0 = (TKey *)w; w += b_k;
     TKey *k1 = (TKey *)w; w += b_k;
     uint32_t *v1 = (uint32_t *)w; w += b_v;
-    uint32_t *inst_gauss = (uint32_t *)w; w += b_v;
     void *tmp = w;
 
     if (n_inst == 0) {
@@ -197,35 +213,35 @@ static int bin_sort_impl(const uint32_t *tiles, const uint64_t *depth_key, const
     VEGS_CUDA(cudaMemcpyAsync(dk0, depth_key, sizeof(uint64_t) * n, cudaMemcpyDeviceToDevice, s));
     iota_kernel<<<(int)((n + 255) / 256), 256, 0, s>>>(id0, n);
     VEGS_CHECK_LAUNCH();
+    cub::DoubleBuffer<uint64_t> dk(dk0, dk1);
+    cub::DoubleBuffer<uint32_t> dv(id0, id1);
     {
-        cub::DoubleBuffer<uint64_t> dk(dk0, dk1);
-        cub::DoubleBuffer<uint32_t> dv(id0, id1);
         size_t tb = b_tmp;
         VEGS_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tb, dk, dv, (int64_t)n, 0, 64, s));
-        rank_kernel<<<(int)((n_kept + 1 + 255) / 256), 256, 0, s>>>(dv.Current(), tiles, n_kept, rank, count_d);
+        depth_counts_kernel<<<(int)((n_kept + 1 + 255) / 256), 256, 0, s>>>(dv.Current(), tiles, n_kept, count_d);
         VEGS_CHECK_LAUNCH();
     }
-    // 2. instance offsets in depth order, then duplication (tile keys in depth order)
+    // 2. instance offsets in depth order, then duplication (tile keys and splat ids in depth order)
     {
         size_t tb = b_tmp;
         VEGS_CUDA(cub::DeviceScan::ExclusiveSum(tmp, tb, count_d, offs_d, (int64_t)n_kept + 1, s));
     }
-    duplicate_kernel<TKey><<<(int)((n * 32 + 255) / 256), 256, 0, s>>>(tiles, rect, offsets, rank, offs_d, n,
-                                                                       tiles_x, k0, inst_pid, inst_gauss);
+    duplicate_kernel<TKey><<<(int)((n_kept + 255) / 256), 256, 0, s>>>(dv.Current(), tiles, (const int4 *)rect,
+                                                                       offs_d, n_kept, tiles_x, k0, sorted_gauss);
     VEGS_CHECK_LAUNCH();
-    // 3. stable sort on the tile id only
+    // 3. stable sort on the tile id only; the values are the splat ids themselves
     cub::DoubleBuffer<TKey> ik(k0, k1);
-    cub::DoubleBuffer<uint32_t> iv(inst_pid, v1);
+    cub::DoubleBuffer<uint32_t> iv(sorted_gauss, v1);
     {
         size_t tb = b_tmp;
         VEGS_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tb, ik, iv, (int64_t)n_inst, 0, tile_bits, s));
     }
-    if (iv.Current() != inst_pid)
-        VEGS_CUDA(cudaMemcpyAsync(inst_pid, iv.Current(), sizeof(uint32_t) * n_inst, cudaMemcpyDeviceToDevice, s));
-    // 4. gauss ids, kept-index order, tile ranges
-    finalize_kernel<TKey><<<(int)((n_inst + 255) / 256), 256, 0, s>>>(ik.Current(), inst_pid, inst_gauss, kept_idx,
-                                                                      n_inst, n_tiles, sorted_gauss, order,
-                                                                      tile_start, tile_end);
+    if (iv.Current() != sorted_gauss)
+        VEGS_CUDA(cudaMemcpyAsync(sorted_gauss, iv.Current(), sizeof(uint32_t) * n_inst, cudaMemcpyDeviceToDevice, s));
+    // 4. duplicate-order indices, kept-index order, tile ranges
+    finalize_kernel<TKey><<<(int)((n_inst + 255) / 256), 256, 0, s>>>(ik.Current(), sorted_gauss, (const int4 *)rect,
+                                                                      offsets, kept_idx, n_inst, n_tiles, tiles_x,
+                                                                      inst_pid, order, tile_start, tile_end);
     VEGS_CHECK_LAUNCH();
     return VEGS_OK;
 }

@@ -328,12 +328,13 @@ __global__ void __launch_bounds__(256) table_from_arrays_kernel(
 // ---------------------------------------------------------------------------------
 // Backward, part 1: float64 sum of each kept Gaussian's instance rows, in duplicate order
 // (== sorted-instance order per splat, the order np.add.at applies at pipeline.py:313-316).
-// A lean kernel (few registers, full occupancy, 16-byte loads) so the ~1 GB of rows per
-// 1024^2 view streams near bandwidth; the register-heavy chain runs separately.
+// A lean kernel (few registers, full occupancy, 16-byte loads); the visited bitmask
+// (L2-resident, one bit per instance) means only the ~30% of rows a pixel actually
+// blended are read.  The register-heavy chain runs separately.
 
 template <typename Real, int NV>
 __global__ void __launch_bounds__(256) reduce_rows_kernel(const uint32_t *tiles, const int64_t *offsets,
-                                                          const Real *rows, int64_t n, uint64_t stamp,
+                                                          const Real *rows, int64_t n, const uint32_t *visited,
                                                           double *sums) {
     const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (g >= n) return;
@@ -341,19 +342,27 @@ __global__ void __launch_bounds__(256) reduce_rows_kernel(const uint32_t *tiles,
     if (cnt == 0) return;
     constexpr int RS = ((7 + (NV - 6)) + 3) & ~3;
     constexpr int NF4 = (int)(RS * sizeof(Real) / 16);
-    const uint32_t s_lo = (uint32_t)stamp, s_hi = (uint32_t)(stamp >> 32);
     double acc[NV];
 #pragma unroll
     for (int k = 0; k < NV; ++k) acc[k] = 0.0;
-    const float4 *src = reinterpret_cast<const float4 *>(rows + (int64_t)RS * offsets[g]);
-    for (uint32_t i = 0; i < cnt; ++i, src += NF4) {
-        Real row[RS];
+    // ascending duplicate-order index; only rows whose visited bit is set were written
+    const int64_t p0 = offsets[g], pend = p0 + cnt;
+    for (int64_t p = p0; p < pend;) {
+        const uint32_t sh = (uint32_t)(p & 31);
+        const int64_t span = (32 - sh) < (pend - p) ? (32 - sh) : (pend - p);
+        uint32_t w = __ldg(visited + (p >> 5)) >> sh;
+        if (span < 32) w &= (1u << span) - 1u;
+        while (w) {
+            const int b = __ffs(w) - 1;
+            w &= w - 1;
+            const float4 *src = reinterpret_cast<const float4 *>(rows + (int64_t)RS * (p + b));
+            Real row[RS];
 #pragma unroll
-        for (int k = 0; k < NF4; ++k) reinterpret_cast<float4 *>(row)[k] = __ldg(src + k);
-        const uint32_t *tag = reinterpret_cast<const uint32_t *>(&row[NV]);
-        if (tag[0] != s_lo || tag[1] != s_hi) continue;  // instance not visited: contributes 0
+            for (int k = 0; k < NF4; ++k) reinterpret_cast<float4 *>(row)[k] = __ldg(src + k);
 #pragma unroll
-        for (int k = 0; k < NV; ++k) acc[k] = acc[k] + (double)row[k];
+            for (int k = 0; k < NV; ++k) acc[k] = acc[k] + (double)row[k];
+        }
+        p += span;
     }
 #pragma unroll
     for (int k = 0; k < NV; ++k) sums[(int64_t)NV * g + k] = acc[k];
@@ -654,7 +663,7 @@ extern "C" int vegs_preprocess_backward(const double *params, int64_t n, const V
                                         int32_t store_f64, const uint32_t *tiles, const int64_t *offsets,
                                         const void *inst_rows, double scale, int32_t accumulate,
                                         double *grads, double *viewspace_norm, uint8_t *visible,
-                                        double *densify_stats, uint64_t row_stamp, void *ws, size_t *ws_bytes,
+                                        double *densify_stats, const uint32_t *inst_visited, void *ws, size_t *ws_bytes,
                                         void *stream) {
     if (!ws_bytes || (n_channels != 3 && n_channels != 11)) return VEGS_ERR_ARG;
     const size_t need = sizeof(double) * (size_t)row_width(n_channels) * (size_t)(n > 0 ? n : 1);
@@ -663,18 +672,18 @@ extern "C" int vegs_preprocess_backward(const double *params, int64_t n, const V
         return VEGS_OK;
     }
     if (*ws_bytes < need) return VEGS_ERR_CAPACITY;
-    if (!cam || !st || !tf_ok(tf) || (n > 0 && (!params || !tiles || !offsets || !grads || !inst_rows)))
+    if (!cam || !st || !tf_ok(tf) || (n > 0 && (!params || !tiles || !offsets || !grads || !inst_rows || !inst_visited)))
         return VEGS_ERR_ARG;
     if (n == 0) return VEGS_OK;
     const int blocks = (int)((n + 255) / 256);
     cudaStream_t s = (cudaStream_t)stream;
     double *sums = (double *)ws;
     if (store_f64) {
-        if (n_channels == 3) reduce_rows_kernel<double, 9><<<blocks, 256, 0, s>>>(tiles, offsets, (const double *)inst_rows, n, row_stamp, sums);
-        else reduce_rows_kernel<double, 17><<<blocks, 256, 0, s>>>(tiles, offsets, (const double *)inst_rows, n, row_stamp, sums);
+        if (n_channels == 3) reduce_rows_kernel<double, 9><<<blocks, 256, 0, s>>>(tiles, offsets, (const double *)inst_rows, n, inst_visited, sums);
+        else reduce_rows_kernel<double, 17><<<blocks, 256, 0, s>>>(tiles, offsets, (const double *)inst_rows, n, inst_visited, sums);
     } else {
-        if (n_channels == 3) reduce_rows_kernel<float, 9><<<blocks, 256, 0, s>>>(tiles, offsets, (const float *)inst_rows, n, row_stamp, sums);
-        else reduce_rows_kernel<float, 17><<<blocks, 256, 0, s>>>(tiles, offsets, (const float *)inst_rows, n, row_stamp, sums);
+        if (n_channels == 3) reduce_rows_kernel<float, 9><<<blocks, 256, 0, s>>>(tiles, offsets, (const float *)inst_rows, n, inst_visited, sums);
+        else reduce_rows_kernel<float, 17><<<blocks, 256, 0, s>>>(tiles, offsets, (const float *)inst_rows, n, inst_visited, sums);
     }
     VEGS_CHECK_LAUNCH();
     const size_t smem = tf_smem_bytes(*tf);

@@ -159,7 +159,7 @@ class Frame:
     out_last: torch.Tensor
     n_contrib: torch.Tensor
     api: dict = field(default_factory=dict)
-    row_stamp: int = 0
+    visited: torch.Tensor | None = None  # per-instance bitmask of the latest backward_rows
 
     @property
     def real(self):
@@ -314,11 +314,11 @@ class Rasterizer:
             d_alpha = A.get("zero_alpha", fr.width * fr.height, fr.real)
             d_alpha.zero_()
         d_img, d_alpha = d_img.contiguous(), d_alpha.contiguous()  # referenced until enqueued
-        fr.row_stamp = _lib.next_stamp()
+        fr.visited = A.get("visited", (max(fr.n_inst, 1) + 31) // 32, torch.int32)
         self._run("vegs_composite_backward", _p(fr.tile_start), _p(fr.tile_end), _p(fr.sorted_gauss), _p(fr.inst_pid),
              _p(fr.record), _p(fr.rect), fr.n_ch, int(fr.store_f64), fr.bg, fr.width, fr.height,
              float(self.settings.alpha_clamp), _p(fr.out_t), _p(fr.out_last), _p(d_img),
-             _p(d_alpha), _p(rows), ctypes.c_uint64(fr.row_stamp), _stream())
+             _p(d_alpha), _p(rows), _p(fr.visited), fr.n_inst, _stream())
         return rows
 
     def backward(self, fr: Frame, d_img: torch.Tensor, d_alpha: torch.Tensor | None = None,
@@ -333,7 +333,7 @@ class Rasterizer:
             grads = torch.empty(19 * fr.n, dtype=torch.float64, device=self.device)
         args = (_p(fr.params), fr.n, ctypes.byref(fr.cam), ctypes.byref(fr.tf.struct), ctypes.byref(fr.settings),
                 fr.n_ch, int(fr.store_f64), _p(fr.tiles), _p(fr.offsets), _p(rows), float(scale), int(accumulate),
-                _p(grads), _p(viewspace_norm), _p(visible), _p(densify_stats), ctypes.c_uint64(fr.row_stamp))
+                _p(grads), _p(viewspace_norm), _p(visible), _p(densify_stats), _p(fr.visited))
         wsz = _lib.size_query("vegs_preprocess_backward", *args, tail=(_stream(),))
         ws = self._alloc().get("ws_pbwd", wsz, torch.uint8)
         self._run("vegs_preprocess_backward", *args, _p(ws), ctypes.byref(ctypes.c_size_t(wsz)), _stream())
