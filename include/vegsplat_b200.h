@@ -126,36 +126,43 @@ int vegs_bin_count(const uint32_t *tiles, int64_t n, int64_t *offsets, int64_t *
                    int64_t *counts, void *ws, size_t *ws_bytes, void *stream);
 
 /* Duplicate + radix sort on (tile, depth rank) == np.lexsort((depth, tile)).
- * Outputs (n_inst): sorted_gauss (Gaussian id), inst_pid (duplicate-order index),
- * order (kept index, the reference's `order`; may be NULL); tile_start/tile_end (n_tiles). */
+ * Outputs (n_inst): sorted_gauss (Gaussian id); optional (may be NULL): inst_pid
+ * (duplicate-order index) and order (kept index, the reference's `order`);
+ * tile_start/tile_end (n_tiles); optional tile_order (n_tiles): tile ids by decreasing
+ * instance count, the launch order the compositing kernels accept (scheduling only). */
 int vegs_bin_sort(const uint32_t *tiles, const uint64_t *depth_key, const int32_t *rect,
                   const int64_t *offsets, const int64_t *kept_idx, int64_t n, int64_t n_kept,
                   int64_t n_inst, int32_t width, int32_t height, int32_t tile_size,
                   uint32_t *sorted_gauss, uint32_t *inst_pid, int64_t *order,
-                  int32_t *tile_start, int32_t *tile_end, void *ws, size_t *ws_bytes,
-                  void *stream);
+                  int32_t *tile_start, int32_t *tile_end, int32_t *tile_order, void *ws,
+                  size_t *ws_bytes, void *stream);
 
 /* ---- composite -------------------------------------------------------------------- */
 /* Tile blend on the splat table.  out_img H x W x C, out_t H x W (storage type),
- * out_last H x W int32 (sorted-instance index, -1 = none), n_contrib H x W int32. */
+ * out_last H x W int32 (sorted-instance index, -1 = none), n_contrib H x W int32.
+ * tile_order (may be NULL) only permutes the order tiles are launched in. */
 int vegs_composite_forward(const int32_t *tile_start, const int32_t *tile_end,
                            const uint32_t *sorted_gauss, const void *record, const int32_t *rect,
                            int32_t n_channels, int32_t store_f64, const double *bg, int32_t width,
                            int32_t height, double alpha_clamp, double trans_stop, void *out_img,
-                           void *out_t, int32_t *out_last, int32_t *n_contrib, void *stream);
+                           void *out_t, int32_t *out_last, int32_t *n_contrib,
+                           const int32_t *tile_order, void *stream);
 
-/* Backward tile blend.  d_img H x W x C, d_alpha H x W (storage type).  Writes per-
- * instance rows [g_mx, g_my, g_ca, g_cb, g_cc, g_alpha, g_ch..., pad] (row stride
- * rec_stride) at the instance's duplicate-order index p = inst_pid[s] and sets bit p of
+/* Backward tile blend.  d_img H x W x C, d_alpha H x W (storage type).  offsets: the
+ * per-Gaussian instance offsets of vegs_bin_count.  Writes per-instance rows [g_mx, g_my,
+ * g_ca, g_cb, g_cc, g_alpha, g_ch..., pad] (row stride rec_stride) at the instance's
+ * duplicate-order index p (offsets[g] + the tile's row-major position in the splat's
+ * tile rectangle; == the inst_pid output of vegs_bin_sort) and sets bit p of
  * inst_visited (ceil(n_inst / 32) words, zeroed by this call).  Rows of instances no
  * pixel blended are not written; vegs_preprocess_backward reads only visited rows. */
 int vegs_composite_backward(const int32_t *tile_start, const int32_t *tile_end,
-                            const uint32_t *sorted_gauss, const uint32_t *inst_pid,
+                            const uint32_t *sorted_gauss, const int64_t *offsets,
                             const void *record, const int32_t *rect, int32_t n_channels,
                             int32_t store_f64, const double *bg, int32_t width, int32_t height,
                             double alpha_clamp, const void *out_t, const int32_t *out_last,
                             const void *d_img, const void *d_alpha, void *inst_rows,
-                            uint32_t *inst_visited, int64_t n_inst, void *stream);
+                            uint32_t *inst_visited, int64_t n_inst, const int32_t *tile_order,
+                            void *stream);
 
 /* Per-Gaussian: float64 reduction of its instance rows (duplicate order == np.add.at
  * order), then projection and shading backward.  grads: flat float64 class-major

@@ -55,12 +55,12 @@ _SIGS = {
     "vegs_splat_table_from_arrays": [P, P, P, P, P, P, c_int64, POINTER(VegsSettings), c_int32, c_int32,
                                      POINTER(VegsSplatTable), P],
     "vegs_bin_count": [P, c_int64, P, P, P, P, POINTER(c_size_t), P],
-    "vegs_bin_sort": [P, P, P, P, P, c_int64, c_int64, c_int64, c_int32, c_int32, c_int32, P, P, P, P, P, P,
+    "vegs_bin_sort": [P, P, P, P, P, c_int64, c_int64, c_int64, c_int32, c_int32, c_int32, P, P, P, P, P, P, P,
                       POINTER(c_size_t), P],
     "vegs_composite_forward": [P, P, P, P, P, c_int32, c_int32, P, c_int32, c_int32, c_double, c_double,
-                               P, P, P, P, P],
+                               P, P, P, P, P, P],
     "vegs_composite_backward": [P, P, P, P, P, P, c_int32, c_int32, P, c_int32, c_int32, c_double, P, P,
-                                P, P, P, P, c_int64, P],
+                                P, P, P, P, c_int64, P, P],
     "vegs_preprocess_backward": [P, c_int64, POINTER(VegsCamera), POINTER(VegsTF), POINTER(VegsSettings),
                                  c_int32, c_int32, P, P, P, c_double, c_int32, P, P, P, P, P, P,
                                  POINTER(c_size_t), P],

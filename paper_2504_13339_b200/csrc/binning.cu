@@ -60,7 +60,7 @@ __global__ void depth_counts_kernel(const uint32_t *sorted_ids, const uint32_t *
     count_d[i] = i == n_kept ? 0u : tiles[sorted_ids[i]];
 }
 
-struct SplatSpan {  // the splat's tile rectangle (pipeline.py:174-180)
+struct SplatSpan {  // the splat's tile rectangle (pipeline.py:174-180); see dup_index
     int x0, y0, nx;
 };
 __device__ __forceinline__ SplatSpan splat_span(int4 r) {
@@ -101,10 +101,11 @@ __global__ void duplicate_kernel(const uint32_t *sorted_ids, const uint32_t *til
     }
 }
 
-// For each sorted instance: its duplicate-order index p = offsets[g] + (row-major index of
-// the tile inside the splat's tile rectangle), optional kept index (`order`), and the
-// searchsorted tile ranges (empty tiles get start == end == insertion point).  The
-// per-splat gathers hit arrays of n entries (L2-resident).
+// For each sorted instance: the searchsorted tile ranges (empty tiles get start == end ==
+// insertion point) and, only when asked for (reference-shaped API), the kept index
+// (`order`) and the duplicate-order index p = offsets[g] + (row-major index of the tile
+// inside the splat's tile rectangle).  The compositing kernels recompute p themselves, so
+// the training path reads 2 bytes per instance here.
 template <typename TKey>
 __global__ void finalize_kernel(const TKey *keys, const uint32_t *sorted_gauss, const int4 *rect,
                                 const int64_t *offsets, const int64_t *kept_idx, int64_t n_inst, int n_tiles,
@@ -112,12 +113,15 @@ __global__ void finalize_kernel(const TKey *keys, const uint32_t *sorted_gauss, 
                                 int32_t *tile_end) {
     const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (s >= n_inst) return;
-    const uint32_t gid = sorted_gauss[s];
     const int tile = (int)keys[s];
-    const SplatSpan sp = splat_span(__ldg(rect + gid));
-    const int ty = tile / tiles_x, tx = tile - ty * tiles_x;
-    inst_pid[s] = (uint32_t)(__ldg(offsets + gid) + (ty - sp.y0) * sp.nx + (tx - sp.x0));
-    if (order) order[s] = kept_idx[gid];
+    if (inst_pid || order) {
+        const uint32_t gid = sorted_gauss[s];
+        if (inst_pid) {
+            const int ty = tile / tiles_x, tx = tile - ty * tiles_x;
+            inst_pid[s] = (uint32_t)dup_index(__ldg(offsets + gid), __ldg(rect + gid), tx, ty);
+        }
+        if (order) order[s] = kept_idx[gid];
+    }
     const int prev = s > 0 ? (int)keys[s - 1] : -1;
     if (tile != prev) {
         for (int t = prev + 1; t <= tile; ++t) tile_start[t] = (int32_t)s;
@@ -127,6 +131,18 @@ __global__ void finalize_kernel(const TKey *keys, const uint32_t *sorted_gauss, 
         for (int t = tile; t < n_tiles; ++t) tile_end[t] = (int32_t)n_inst;
         for (int t = tile + 1; t < n_tiles; ++t) tile_start[t] = (int32_t)n_inst;
     }
+}
+
+// Scheduling key of each tile: instance count (capped at 16 bits), complemented so an
+// ascending sort puts the heaviest tiles first (the compositing grids then start the
+// longest tiles earliest).
+__global__ void tile_weight_kernel(const int32_t *tile_start, const int32_t *tile_end, int n_tiles, uint32_t *key,
+                                   int32_t *val) {
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= n_tiles) return;
+    const uint32_t c = (uint32_t)(tile_end[t] - tile_start[t]);
+    key[t] = 0xffffu - (c < 0xffffu ? c : 0xffffu);
+    val[t] = t;
 }
 
 static size_t align_up(size_t x) { return (x + 255) & ~size_t(255); }
@@ -167,10 +183,10 @@ template <typename TKey>
 static int bin_sort_impl(const uint32_t *tiles, const uint64_t *depth_key, const int32_t *rect,
                          const int64_t *offsets, const int64_t *kept_idx, int64_t n, int64_t n_kept,
                          int64_t n_inst, int tiles_x, int n_tiles, uint32_t *sorted_gauss, uint32_t *inst_pid,
-                         int64_t *order, int32_t *tile_start, int32_t *tile_end, void *ws, size_t *ws_bytes,
-                         cudaStream_t s) {
+                         int64_t *order, int32_t *tile_start, int32_t *tile_end, int32_t *tile_order, void *ws,
+                         size_t *ws_bytes, cudaStream_t s) {
     const int tile_bits = bits_for(n_tiles);
-    size_t t_depth = 0, t_scan = 0, t_inst = 0;
+    size_t t_depth = 0, t_scan = 0, t_inst = 0, t_tiles = 0;
     {
         cub::DoubleBuffer<uint64_t> dk(nullptr, nullptr);
         cub::DoubleBuffer<uint32_t> dv(nullptr, nullptr);
@@ -180,13 +196,18 @@ static int bin_sort_impl(const uint32_t *tiles, const uint64_t *depth_key, const
         cub::DoubleBuffer<TKey> ik(nullptr, nullptr);
         cub::DoubleBuffer<uint32_t> iv(nullptr, nullptr);
         VEGS_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, t_inst, ik, iv, (int64_t)n_inst, 0, tile_bits, s));
+        uint32_t *tk = nullptr;
+        int32_t *tv = nullptr;
+        VEGS_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, t_tiles, tk, tk, tv, tv, n_tiles, 0, 16, s));
     }
     const size_t b_dk = align_up(sizeof(uint64_t) * n), b_id = align_up(sizeof(uint32_t) * (n + 1));
     const size_t b_k = align_up(sizeof(TKey) * n_inst), b_v = align_up(sizeof(uint32_t) * n_inst);
     size_t t_max = t_depth > t_inst ? t_depth : t_inst;
     t_max = t_max > t_scan ? t_max : t_scan;
+    t_max = t_max > t_tiles ? t_max : t_tiles;
     const size_t b_tmp = align_up(t_max);
-    const size_t need = 2 * b_dk + 4 * b_id + 2 * b_k + b_v + b_tmp;
+    const size_t b_t = align_up(sizeof(uint32_t) * n_tiles);
+    const size_t need = 2 * b_dk + 4 * b_id + 2 * b_k + b_v + 3 * b_t + b_tmp;
     if (!ws) {
         *ws_bytes = need;
         return VEGS_OK;
@@ -202,11 +223,18 @@ static int bin_sort_impl(const uint32_t *tiles, const uint64_t *depth_key, const
     TKey *k0 = (TKey *)w; w += b_k;
     TKey *k1 = (TKey *)w; w += b_k;
     uint32_t *v1 = (uint32_t *)w; w += b_v;
+    uint32_t *tkey0 = (uint32_t *)w; w += b_t;
+    uint32_t *tkey1 = (uint32_t *)w; w += b_t;
+    int32_t *tval = (int32_t *)w; w += b_t;
     void *tmp = w;
 
     if (n_inst == 0) {
         VEGS_CUDA(cudaMemsetAsync(tile_start, 0, sizeof(int32_t) * n_tiles, s));
         VEGS_CUDA(cudaMemsetAsync(tile_end, 0, sizeof(int32_t) * n_tiles, s));
+        if (tile_order) {
+            tile_weight_kernel<<<(n_tiles + 255) / 256, 256, 0, s>>>(tile_start, tile_end, n_tiles, tkey0, tile_order);
+            VEGS_CHECK_LAUNCH();
+        }
         return VEGS_OK;
     }
     // 1. stable depth order of the kept splats (culled ones carry the max key, sort last)
@@ -243,6 +271,13 @@ static int bin_sort_impl(const uint32_t *tiles, const uint64_t *depth_key, const
                                                                       offsets, kept_idx, n_inst, n_tiles, tiles_x,
                                                                       inst_pid, order, tile_start, tile_end);
     VEGS_CHECK_LAUNCH();
+    // 5. optional launch order for the compositing kernels: heaviest tiles first
+    if (tile_order) {
+        tile_weight_kernel<<<(n_tiles + 255) / 256, 256, 0, s>>>(tile_start, tile_end, n_tiles, tkey0, tval);
+        VEGS_CHECK_LAUNCH();
+        size_t tb = b_tmp;
+        VEGS_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tb, tkey0, tkey1, tval, tile_order, n_tiles, 0, 16, s));
+    }
     return VEGS_OK;
 }
 
@@ -250,18 +285,19 @@ extern "C" int vegs_bin_sort(const uint32_t *tiles, const uint64_t *depth_key, c
                              const int64_t *offsets, const int64_t *kept_idx, int64_t n, int64_t n_kept,
                              int64_t n_inst, int32_t width, int32_t height, int32_t tile_size,
                              uint32_t *sorted_gauss, uint32_t *inst_pid, int64_t *order,
-                             int32_t *tile_start, int32_t *tile_end, void *ws, size_t *ws_bytes,
-                             void *stream) {
+                             int32_t *tile_start, int32_t *tile_end, int32_t *tile_order, void *ws,
+                             size_t *ws_bytes, void *stream) {
     if (!ws_bytes || tile_size != kTile || width < 1 || height < 1) return VEGS_ERR_ARG;
     if (n_inst >= (int64_t(1) << 32) || n >= (int64_t(1) << 32)) return VEGS_ERR_ARG;
     if (ws && (n > 0) && (!tiles || !depth_key || !rect || !offsets || !kept_idx)) return VEGS_ERR_ARG;
-    if (ws && (!tile_start || !tile_end || (n_inst > 0 && (!sorted_gauss || !inst_pid)))) return VEGS_ERR_ARG;
+    if (ws && (!tile_start || !tile_end || (n_inst > 0 && !sorted_gauss))) return VEGS_ERR_ARG;
     const int tiles_x = (width + kTile - 1) / kTile, tiles_y = (height + kTile - 1) / kTile;
     const int n_tiles = tiles_x * tiles_y;
     cudaStream_t s = (cudaStream_t)stream;
     if (n_tiles <= 65536)
         return bin_sort_impl<uint16_t>(tiles, depth_key, rect, offsets, kept_idx, n, n_kept, n_inst, tiles_x,
-                                       n_tiles, sorted_gauss, inst_pid, order, tile_start, tile_end, ws, ws_bytes, s);
+                                       n_tiles, sorted_gauss, inst_pid, order, tile_start, tile_end, tile_order, ws,
+                                       ws_bytes, s);
     return bin_sort_impl<uint32_t>(tiles, depth_key, rect, offsets, kept_idx, n, n_kept, n_inst, tiles_x, n_tiles,
-                                   sorted_gauss, inst_pid, order, tile_start, tile_end, ws, ws_bytes, s);
+                                   sorted_gauss, inst_pid, order, tile_start, tile_end, tile_order, ws, ws_bytes, s);
 }

@@ -245,7 +245,13 @@ __device__ void write_record(Real *r, double px, double py, const double *conic,
 // ---------------------------------------------------------------------------------
 
 template <typename Real>
-__global__ void __launch_bounds__(256) preprocess_fwd_kernel(
+#ifndef VEGS_PFWD_MINB
+#define VEGS_PFWD_MINB 4  // 64 registers: 4x the resident warps of the unbounded build, ~2x faster
+#endif
+#ifndef VEGS_PBWD_MINB
+#define VEGS_PBWD_MINB 4
+#endif
+__global__ void __launch_bounds__(256, VEGS_PFWD_MINB) preprocess_fwd_kernel(
     const double *params, int64_t n, VegsCamera cam, VegsTF tf, VegsSettings st, int n_ch,
     VegsSplatTable out) {
     extern __shared__ double tf_smem[];
@@ -352,15 +358,28 @@ __global__ void __launch_bounds__(256) reduce_rows_kernel(const uint32_t *tiles,
         const int64_t span = (32 - sh) < (pend - p) ? (32 - sh) : (pend - p);
         uint32_t w = __ldg(visited + (p >> 5)) >> sh;
         if (span < 32) w &= (1u << span) - 1u;
-        while (w) {
-            const int b = __ffs(w) - 1;
-            w &= w - 1;
-            const float4 *src = reinterpret_cast<const float4 *>(rows + (int64_t)RS * (p + b));
-            Real row[RS];
+        while (w) {  // up to 4 visited rows in flight per round, summed in ascending order
+            constexpr int Q = RS * sizeof(Real) <= 48 ? 4 : 1;  // rgb float32 rows: 4 in flight
+            int b[Q];
 #pragma unroll
-            for (int k = 0; k < NF4; ++k) reinterpret_cast<float4 *>(row)[k] = __ldg(src + k);
+            for (int q = 0; q < Q; ++q) {
+                b[q] = w ? __ffs(w) - 1 : -1;
+                w &= w - 1;
+            }
+            Real row[Q][RS];
 #pragma unroll
-            for (int k = 0; k < NV; ++k) acc[k] = acc[k] + (double)row[k];
+            for (int q = 0; q < Q; ++q)
+                if (b[q] >= 0) {
+                    const float4 *src = reinterpret_cast<const float4 *>(rows + (int64_t)RS * (p + b[q]));
+#pragma unroll
+                    for (int k = 0; k < NF4; ++k) reinterpret_cast<float4 *>(row[q])[k] = __ldg(src + k);
+                }
+#pragma unroll
+            for (int q = 0; q < Q; ++q)
+                if (b[q] >= 0) {
+#pragma unroll
+                    for (int k = 0; k < NV; ++k) acc[k] = acc[k] + (double)row[q][k];
+                }
         }
         p += span;
     }
@@ -370,7 +389,7 @@ __global__ void __launch_bounds__(256) reduce_rows_kernel(const uint32_t *tiles,
 
 // Backward, part 2: projection and shading adjoints per Gaussian (float64).
 
-__global__ void __launch_bounds__(256) preprocess_bwd_kernel(
+__global__ void __launch_bounds__(256, VEGS_PBWD_MINB) preprocess_bwd_kernel(
     const double *params, int64_t n, VegsCamera cam, VegsTF tf, VegsSettings st, int n_ch,
     const uint32_t *tiles, const double *sums, double scale, int accumulate,
     double *grads, double *vs_norm, uint8_t *visible_out, double *dstats) {

@@ -53,6 +53,14 @@ __device__ __forceinline__ void tile_pixel(int tid, int &lx, int &ly) {
     ly = (warp >> 1) * 4 + (lane >> 3);
 }
 
+// Duplicate-order index of a splat's instance in tile (tx, ty): the splat's first index
+// (exclusive scan of tile counts) plus the tile's row-major position inside the splat's
+// tile rectangle (pipeline.py:174-187).  rect = (x0, x1, y0, y1) in pixels, clipped.
+__device__ __forceinline__ int64_t dup_index(int64_t first, int4 r, int tx, int ty) {
+    const int x0 = r.x / kTile, y0 = r.z / kTile, nx = (r.y - 1) / kTile - x0 + 1;
+    return first + (int64_t)(ty - y0) * nx + (tx - x0);
+}
+
 template <typename T>
 __device__ __forceinline__ T warp_sum(T v) {
 #pragma unroll

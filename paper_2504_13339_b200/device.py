@@ -37,8 +37,9 @@ LAUNCHES = {
     "vegs_preprocess_forward": 1,
     "vegs_splat_table_from_arrays": 1,
     "vegs_bin_count": 4,          # pack, CUB scan (init + sweep), unpack
-    "vegs_bin_sort": 20,          # iota, CUB depth sort (hist + scan + 8 onesweep), rank, duplicate,
-                                  # CUB key sort (hist + scan + 4 onesweep), finalize
+    "vegs_bin_sort": 22,          # iota, CUB depth sort (hist + scan + 8 onesweep), depth counts, scan (2), duplicate,
+                                  # CUB key sort (hist + scan + 2 onesweep), finalize, tile weights +
+                                  # single-tile CUB sort (heaviest-first tile order)
     "vegs_composite_forward": 1,
     "vegs_composite_backward": 1,
     "vegs_preprocess_backward": 2,  # row reduction + chain
@@ -150,10 +151,11 @@ class Frame:
     n_kept: int
     n_inst: int
     sorted_gauss: torch.Tensor
-    inst_pid: torch.Tensor
+    inst_pid: torch.Tensor | None  # duplicate-order index per sorted instance (API path only)
     order: torch.Tensor | None
     tile_start: torch.Tensor
     tile_end: torch.Tensor
+    tile_order: torch.Tensor | None  # heaviest-first launch order of the compositing kernels
     out_img: torch.Tensor
     out_t: torch.Tensor
     out_last: torch.Tensor
@@ -279,12 +281,13 @@ class Rasterizer:
         tiles_x = (width + TILE - 1) // TILE
         n_tiles = tiles_x * ((height + TILE - 1) // TILE)
         sorted_gauss = A.get("sorted_gauss", n_inst, torch.int32)
-        inst_pid = A.get("inst_pid", n_inst, torch.int32)
+        inst_pid = A.get("inst_pid", n_inst, torch.int32) if want_order else None
         order = A.get("order", n_inst, torch.int64) if want_order else None
         tile_start = A.get("tile_start", n_tiles, torch.int32)
         tile_end = A.get("tile_end", n_tiles, torch.int32)
+        tile_order = A.get("tile_order", n_tiles, torch.int32)
         args = (_p(tiles), _p(depth_key), _p(rect), _p(offsets), _p(kept_idx), n, n_kept, n_inst, width, height,
-                TILE, _p(sorted_gauss), _p(inst_pid), _p(order), _p(tile_start), _p(tile_end))
+                TILE, _p(sorted_gauss), _p(inst_pid), _p(order), _p(tile_start), _p(tile_end), _p(tile_order))
         wsz = _lib.size_query("vegs_bin_sort", *args, tail=(s,))
         ws = A.get("ws_sort", wsz, torch.uint8)
         self._run("vegs_bin_sort", *args, _p(ws), ctypes.byref(ctypes.c_size_t(wsz)), s)
@@ -296,12 +299,13 @@ class Rasterizer:
         bg = (ctypes.c_double * 3)(*[float(x) for x in background])
         self._run("vegs_composite_forward", _p(tile_start), _p(tile_end), _p(sorted_gauss), _p(record), _p(rect),
              self.n_ch, int(self.store_f64), bg, width, height, float(self.settings.alpha_clamp),
-             float(self.settings.transmittance_stop), _p(out_img), _p(out_t), _p(out_last), _p(n_contrib), s)
+             float(self.settings.transmittance_stop), _p(out_img), _p(out_t), _p(out_last), _p(n_contrib),
+             _p(tile_order), s)
         return Frame(n=n, n_ch=self.n_ch, store_f64=self.store_f64, width=width, height=height, cam=cs, tf=tf,
                      settings=self.st, bg=bg, params=params, record=record, rect=rect, tiles=tiles,
                      depth_key=depth_key, offsets=offsets, kept_idx=kept_idx, n_kept=n_kept, n_inst=n_inst,
                      sorted_gauss=sorted_gauss, inst_pid=inst_pid, order=order, tile_start=tile_start,
-                     tile_end=tile_end, out_img=out_img, out_t=out_t, out_last=out_last, n_contrib=n_contrib,
+                     tile_end=tile_end, tile_order=tile_order, out_img=out_img, out_t=out_t, out_last=out_last, n_contrib=n_contrib,
                      api=api)
 
     # -- backward -------------------------------------------------------------------
@@ -315,10 +319,10 @@ class Rasterizer:
             d_alpha.zero_()
         d_img, d_alpha = d_img.contiguous(), d_alpha.contiguous()  # referenced until enqueued
         fr.visited = A.get("visited", (max(fr.n_inst, 1) + 31) // 32, torch.int32)
-        self._run("vegs_composite_backward", _p(fr.tile_start), _p(fr.tile_end), _p(fr.sorted_gauss), _p(fr.inst_pid),
+        self._run("vegs_composite_backward", _p(fr.tile_start), _p(fr.tile_end), _p(fr.sorted_gauss), _p(fr.offsets),
              _p(fr.record), _p(fr.rect), fr.n_ch, int(fr.store_f64), fr.bg, fr.width, fr.height,
              float(self.settings.alpha_clamp), _p(fr.out_t), _p(fr.out_last), _p(d_img),
-             _p(d_alpha), _p(rows), _p(fr.visited), fr.n_inst, _stream())
+             _p(d_alpha), _p(rows), _p(fr.visited), fr.n_inst, _p(fr.tile_order), _stream())
         return rows
 
     def backward(self, fr: Frame, d_img: torch.Tensor, d_alpha: torch.Tensor | None = None,

@@ -1,0 +1,42 @@
+"""Diagnostic: per-tile work of one c2 view (instances up to the tile's last contributor)
+and the makespan of greedy scheduling onto G concurrent CTA slots, in launch order vs
+heaviest-first: python scripts/tile_balance.py"""
+import heapq
+import sys
+from pathlib import Path
+
+import numpy as np
+import torch
+
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+from paper_2504_13339_b200 import scenes  # noqa: E402
+from paper_2504_13339_b200.device import DeviceTF, Rasterizer  # noqa: E402
+
+
+def makespan(work, slots):
+    h = [0.0] * slots
+    for w in work:
+        t = heapq.heappop(h)
+        heapq.heappush(h, t + w)
+    return max(h)
+
+
+def main():
+    gs, truth, tf, cams = scenes.config_scene("c2")
+    rz = Rasterizer()
+    params = torch.from_numpy(gs.pack()).cuda()
+    fr = rz.forward(params, len(gs), DeviceTF(tf), cams[0])
+    ts, te = fr.tile_start.cpu().numpy(), fr.tile_end.cpu().numpy()
+    last = fr.out_last.view(1024, 1024).cpu().numpy()
+    t = last.reshape(64, 16, 64, 16).transpose(0, 2, 1, 3).reshape(4096, 256).max(1)
+    work = np.where(t >= 0, t - ts + 1, 0).astype(np.float64) + 1.0
+    n_inst = (te - ts).astype(np.float64)
+    print("tiles", len(work), "work mean", work.mean(), "max", work.max(), "p50", np.median(work), "inst mean", n_inst.mean())
+    for slots in (148 * 6, 148 * 8):
+        lb = work.sum() / slots
+        nat, lpt = makespan(work, slots), makespan(np.sort(work)[::-1], slots)
+        print(f"slots {slots}: lower bound {lb:.0f}  launch order {nat:.0f} ({nat / lb:.3f})  heaviest-first {lpt:.0f} ({lpt / lb:.3f})")
+
+
+if __name__ == "__main__":
+    main()

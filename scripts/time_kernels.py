@@ -1,6 +1,7 @@
-"""Quick timing of the compositing kernels on one config-2 view (CUDA events, single
-stream): python scripts/time_kernels.py [reps]"""
+"""Quick timing of every C-ABI call of one config-2 view (CUDA events around each call on a
+single stream, forward + backward over 4 views): python scripts/time_kernels.py [reps]"""
 import sys
+from collections import defaultdict
 from pathlib import Path
 
 import torch
@@ -18,24 +19,23 @@ def main():
     rz = Rasterizer()
     params = torch.from_numpy(gs.pack()).cuda()
     grads = torch.zeros_like(params)
-    times = {"vegs_composite_forward": [], "vegs_composite_backward": []}
+    times = defaultdict(list)
 
     class T:
         def mark(self, name, begin, rz=None):
-            if name in times:
-                ev = torch.cuda.Event(enable_timing=True)
-                ev.record()
-                if begin:
-                    self.s = ev
-                else:
-                    times[name].append((self.s, ev))
+            ev = torch.cuda.Event(enable_timing=True)
+            ev.record()
+            if begin:
+                self.s = ev
+            else:
+                times[name].append((self.s, ev))
 
     d_img = torch.rand(1024, 1024, 3, device="cuda") - 0.5
     for r in range(reps + 2):
         rz.timer = T() if r >= 2 else None
         for cam in cams[:4]:
             fr = rz.forward(params, len(gs), dtf, cam)
-            rz.backward(fr, d_img, None, grads)
+            rz.backward(fr, d_img, None, grads, accumulate=True)
     torch.cuda.synchronize()
     for k, v in times.items():
         ms = [a.elapsed_time(b) for a, b in v]
