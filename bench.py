@@ -264,17 +264,19 @@ def run_b200(args) -> None:
     render_mpx_s = px / (rms / 1000.0) / 1e6
     del pipe
 
-    # ---- end to end through the public API with host buffers
+    # ---- end to end through the public API with host buffers: the views carry their
+    # targets in pinned host memory; the trainer uploads them (overlapped with compute)
+    # inside the timed region and the loss is read back every step
     h2d = sum(t.numel() * t.element_size() for t in host_targets)
+    host_views = [View(v.camera, v.tf, t) for v, t in zip(views, host_targets)]
+    trainer.step(host_views, total_views=VIEWS_PER_STEP).item()  # warm the upload path
     barrier()
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     s0.record()
     for _ in range(args.steps):
-        for t_dev, t_host in zip(targets, host_targets):
-            t_dev.copy_(t_host, non_blocking=True)
-        lv = trainer.step(views, total_views=VIEWS_PER_STEP).item()  # D2H of the loss
+        lv = trainer.step(host_views, total_views=VIEWS_PER_STEP).item()  # D2H of the loss
     s1.record()
     torch.cuda.synchronize()
     wall = time.perf_counter() - t0

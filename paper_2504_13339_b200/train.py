@@ -160,7 +160,7 @@ class DensifyStats:
 class View:
     camera: object
     tf: DeviceTF
-    target: torch.Tensor  # (H, W, 3) float32 on the device
+    target: torch.Tensor  # (H, W, 3) float32, on the device or in (pinned) host memory
 
 
 class _Lane:
@@ -220,6 +220,10 @@ class Trainer:
                       for i in range(max(1, lanes))]
         self.lanes[0].grads = self.grads
         self.rz = self.lanes[0].rz
+        # host-resident targets are uploaded on their own stream, one event per view, so
+        # the H2D copies overlap the previous views' compositing
+        self._copy_stream = None
+        self._target_bufs: list[torch.Tensor] = []
 
     def set_timer(self, timer) -> None:
         for lane in self.lanes:
@@ -232,17 +236,47 @@ class Trainer:
     def gaussians(self) -> GaussianSet:
         return GaussianSet.unpack(self.params.cpu().numpy(), self.n)
 
-    def _loss_and_backward(self, lane, fr, view: View, scale: float, first: bool, sums: torch.Tensor) -> None:
+    def _upload_targets(self, views: list[View], main) -> list:
+        """Queue the H2D copies of host-resident targets on the copy stream; returns per
+        view (device target, event or None)."""
+        out = []
+        if all(v.target.is_cuda for v in views):
+            return [(v.target, None) for v in views]
+        if self._copy_stream is None:
+            self._copy_stream = torch.cuda.Stream(self.device)
+        cs = self._copy_stream
+        cs.wait_stream(main)  # the previous step's readers of the buffers are done
+        while len(self._target_bufs) < len(views):
+            self._target_bufs.append(torch.empty(0, dtype=torch.float32, device=self.device))
+        for i, v in enumerate(views):
+            if v.target.is_cuda:
+                out.append((v.target, None))
+                continue
+            buf = self._target_bufs[i]
+            if buf.shape != v.target.shape:
+                buf = self._target_bufs[i] = torch.empty(v.target.shape, dtype=v.target.dtype, device=self.device)
+            ev = torch.cuda.Event()
+            with torch.cuda.stream(cs):
+                buf.copy_(v.target, non_blocking=True)
+                ev.record(cs)
+            out.append((buf, ev))
+        return out
+
+    def _loss_and_backward(self, lane, fr, view: View, scale: float, first: bool, sums: torch.Tensor,
+                           target: torch.Tensor | None = None, ready=None) -> None:
         h, w = fr.height, fr.width
         img = fr.out_img.view(h, w, fr.n_ch)
         if lane.d_img is None or lane.d_img.numel() != img.numel():
             lane.d_img = torch.empty_like(img)
-        lane.loss(img, view.target, self.w_l1, self.lam, lane.d_img, sums[:2])
+        target = view.target if target is None else target
+        if ready is not None:
+            lane.stream.wait_event(ready)
+        lane.loss(img, target, self.w_l1, self.lam, lane.d_img, sums[:2])
         lane.loss_launches += 2
         if self.with_aux:
             cam = view.camera
             px_scale = 2.0 * math.tan(0.5 * cam.fov_y) / cam.height
-            lane.loss.aux(img, fr.out_t.view(h, w), view.target, px_scale, self.config.normal_loss_weight,
+            lane.loss.aux(img, fr.out_t.view(h, w), target, px_scale, self.config.normal_loss_weight,
                           self.config.smooth_loss_weight, lane.d_img, sums[2:5])
             lane.loss_launches += 3
         lane.rz.backward(fr, lane.d_img, None, lane.grads, scale=scale, accumulate=not first,
@@ -262,6 +296,7 @@ class Trainer:
             lane.stream.wait_stream(main)  # parameters updated, sums zeroed
         lanes[0].grads = self.grads
         lanes[0].dstats = self.densify_stats
+        targets = self._upload_targets(views, main)
         pend: list = [None] * n_v
         used = [False] * len(lanes)
 
@@ -280,7 +315,7 @@ class Trainer:
             with torch.cuda.stream(lane.stream):
                 fr = lane.rz.forward_end(pend[i])
                 pend[i] = None
-                self._loss_and_backward(lane, fr, views[i], 1.0 / total, not used[k], sums[i])
+                self._loss_and_backward(lane, fr, views[i], 1.0 / total, not used[k], sums[i], *targets[i])
             used[k] = True
         if not used[0]:
             self.grads.zero_()

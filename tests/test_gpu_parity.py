@@ -296,6 +296,29 @@ def test_trainer_step_matches_reference_step():
         assert G.norm_rel(step_gpu, step_ref) <= 1e-3, k
 
 
+def test_trainer_host_targets_match_device_targets():
+    """Views may carry pinned host targets (uploaded on a copy stream inside step()); the
+    step is bitwise the one with device-resident targets."""
+    from paper_2504_13339_b200 import scenes
+    from paper_2504_13339_b200.device import DeviceTF
+    from paper_2504_13339_b200.train import Trainer, TrainConfig, View
+
+    d = G.load("train_step")
+    learned = scenes.random_gaussians(2000, seed=0)
+    dtf = DeviceTF(scenes.random_tf(2, 4))
+    cams = scenes.orbit_cameras(2, 3, 64, 64)
+    host = [torch.from_numpy(d[f"target{i}"]).pin_memory() for i in range(2)]
+    runs = []
+    for on_host in (False, True, True):
+        tr = Trainer(learned, TrainConfig(iterations=100))
+        views = [View(c, dtf, t if on_host else t.cuda()) for c, t in zip(cams, host)]
+        losses = [float(tr.step(views, iteration=it).item()) for it in (1, 2)]
+        runs.append((losses, tr.params.cpu()))
+    for losses, params in runs[1:]:
+        assert losses == runs[0][0]
+        assert torch.equal(params, runs[0][1])
+
+
 # -- full-size properties (config 2 geometry, one view) ---------------------------------
 
 def test_c2_view_properties():
