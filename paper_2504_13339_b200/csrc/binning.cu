@@ -1,8 +1,9 @@
 // Tile binning: the device form of _build_instances (pipeline.py:163-194).
 //
 //   np.repeat over kept splats  ->  one exclusive scan of packed (kept, tiles) counters
-//   np.lexsort((depth, tile))   ->  (1) stable radix sort of the kept splats' float64 depth
-//                                   keys; (2) instances duplicated *in depth order*; (3) a
+//   np.lexsort((depth, tile))   ->  (1) stable depth order of the kept splats (radix sort
+//                                   on float32-rounded keys, exact float64 order restored
+//                                   inside ties); (2) instances duplicated *in depth order*; (3) a
 //                                   stable radix sort on the tile id alone (12-16 bits)
 //   np.searchsorted ranges      ->  boundary scatter over the sorted tile ids
 //
@@ -47,9 +48,44 @@ __global__ void unpack_counts_kernel(const uint64_t *scan, int64_t n, int64_t *o
     }
 }
 
-__global__ void iota_kernel(uint32_t *out, int64_t n) {
+// Coarse 32-bit depth keys: the order-preserving bits of (float)depth.  Rounding to float32
+// is monotone, so sorting by this key and then by the exact float64 key inside runs of
+// equal coarse keys (depth_ties_kernel) is the float64 order; culled splats (key ~0) map
+// to 0xffffffff and still sort last.  Half the radix passes of the 64-bit key.
+__global__ void depth_key32_kernel(const uint64_t *key64, int64_t n, uint32_t *key32, uint32_t *ids) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i < n) out[i] = (uint32_t)i;
+    if (i >= n) return;
+    const uint64_t k = key64[i];
+    uint32_t out = 0xffffffffu;
+    if (k != ~0ull) {
+        const uint64_t b = (k >> 63) ? (k & 0x7fffffffffffffffull) : ~k;  // inverse of depth_order_key
+        const uint32_t f = __float_as_uint((float)__longlong_as_double((long long)b));
+        out = (f >> 31) ? ~f : (f | 0x80000000u);
+    }
+    key32[i] = out;
+    ids[i] = (uint32_t)i;
+}
+
+// Runs of equal coarse keys among the kept splats are re-ordered by the exact float64 key
+// (insertion sort, strict comparison: the stable sort's index order survives among equal
+// float64 depths).  Runs are almost always of length 1-2.
+__global__ void depth_ties_kernel(const uint32_t *key32, const uint64_t *key64, int64_t n_kept, uint32_t *ids) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i + 1 >= n_kept) return;
+    const uint32_t k = key32[i];
+    if (key32[i + 1] != k || (i > 0 && key32[i - 1] == k)) return;  // not the start of a run
+    int64_t j = i + 2;
+    while (j < n_kept && key32[j] == k) ++j;
+    for (int64_t a = i + 1; a < j; ++a) {
+        const uint32_t id = ids[a];
+        const uint64_t ka = key64[id];
+        int64_t b = a - 1;
+        while (b >= i && key64[ids[b]] > ka) {
+            ids[b + 1] = ids[b];
+            --b;
+        }
+        ids[b + 1] = id;
+    }
 }
 
 // tile count of each kept splat in depth order (the scan input for the depth-order offsets)
@@ -188,9 +224,9 @@ static int bin_sort_impl(const uint32_t *tiles, const uint64_t *depth_key, const
     const int tile_bits = bits_for(n_tiles);
     size_t t_depth = 0, t_scan = 0, t_inst = 0, t_tiles = 0;
     {
-        cub::DoubleBuffer<uint64_t> dk(nullptr, nullptr);
+        cub::DoubleBuffer<uint32_t> dk(nullptr, nullptr);
         cub::DoubleBuffer<uint32_t> dv(nullptr, nullptr);
-        VEGS_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, t_depth, dk, dv, (int64_t)n, 0, 64, s));
+        VEGS_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, t_depth, dk, dv, (int64_t)n, 0, 32, s));
         uint32_t *dummy = nullptr;
         VEGS_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, t_scan, dummy, dummy, (int64_t)n_kept + 1, s));
         cub::DoubleBuffer<TKey> ik(nullptr, nullptr);
@@ -200,7 +236,7 @@ static int bin_sort_impl(const uint32_t *tiles, const uint64_t *depth_key, const
         int32_t *tv = nullptr;
         VEGS_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, t_tiles, tk, tk, tv, tv, n_tiles, 0, 16, s));
     }
-    const size_t b_dk = align_up(sizeof(uint64_t) * n), b_id = align_up(sizeof(uint32_t) * (n + 1));
+    const size_t b_dk = align_up(sizeof(uint32_t) * n), b_id = align_up(sizeof(uint32_t) * (n + 1));
     const size_t b_k = align_up(sizeof(TKey) * n_inst), b_v = align_up(sizeof(uint32_t) * n_inst);
     size_t t_max = t_depth > t_inst ? t_depth : t_inst;
     t_max = t_max > t_scan ? t_max : t_scan;
@@ -214,8 +250,8 @@ static int bin_sort_impl(const uint32_t *tiles, const uint64_t *depth_key, const
     }
     if (*ws_bytes < need) return VEGS_ERR_CAPACITY;
     char *w = (char *)ws;
-    uint64_t *dk0 = (uint64_t *)w; w += b_dk;
-    uint64_t *dk1 = (uint64_t *)w; w += b_dk;
+    uint32_t *dk0 = (uint32_t *)w; w += b_dk;
+    uint32_t *dk1 = (uint32_t *)w; w += b_dk;
     uint32_t *id0 = (uint32_t *)w; w += b_id;
     uint32_t *id1 = (uint32_t *)w; w += b_id;
     uint32_t *count_d = (uint32_t *)w; w += b_id;
@@ -237,15 +273,17 @@ static int bin_sort_impl(const uint32_t *tiles, const uint64_t *depth_key, const
         }
         return VEGS_OK;
     }
-    // 1. stable depth order of the kept splats (culled ones carry the max key, sort last)
-    VEGS_CUDA(cudaMemcpyAsync(dk0, depth_key, sizeof(uint64_t) * n, cudaMemcpyDeviceToDevice, s));
-    iota_kernel<<<(int)((n + 255) / 256), 256, 0, s>>>(id0, n);
+    // 1. stable depth order of the kept splats (culled ones carry the max key, sort last):
+    //    radix sort on the coarse 32-bit key, then exact float64 order inside ties
+    depth_key32_kernel<<<(int)((n + 255) / 256), 256, 0, s>>>(depth_key, n, dk0, id0);
     VEGS_CHECK_LAUNCH();
-    cub::DoubleBuffer<uint64_t> dk(dk0, dk1);
+    cub::DoubleBuffer<uint32_t> dk(dk0, dk1);
     cub::DoubleBuffer<uint32_t> dv(id0, id1);
     {
         size_t tb = b_tmp;
-        VEGS_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tb, dk, dv, (int64_t)n, 0, 64, s));
+        VEGS_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tb, dk, dv, (int64_t)n, 0, 32, s));
+        depth_ties_kernel<<<(int)((n_kept + 255) / 256), 256, 0, s>>>(dk.Current(), depth_key, n_kept, dv.Current());
+        VEGS_CHECK_LAUNCH();
         depth_counts_kernel<<<(int)((n_kept + 1 + 255) / 256), 256, 0, s>>>(dv.Current(), tiles, n_kept, count_d);
         VEGS_CHECK_LAUNCH();
     }

@@ -37,7 +37,8 @@ LAUNCHES = {
     "vegs_preprocess_forward": 1,
     "vegs_splat_table_from_arrays": 1,
     "vegs_bin_count": 4,          # pack, CUB scan (init + sweep), unpack
-    "vegs_bin_sort": 22,          # iota, CUB depth sort (hist + scan + 8 onesweep), depth counts, scan (2), duplicate,
+    "vegs_bin_sort": 19,          # coarse keys, CUB depth sort (hist + scan + 4 onesweep), ties, depth counts, scan (2),
+                                  # duplicate,
                                   # CUB key sort (hist + scan + 2 onesweep), finalize, tile weights +
                                   # single-tile CUB sort (heaviest-first tile order)
     "vegs_composite_forward": 1,

@@ -151,3 +151,27 @@ def test_partial_tiles_match_oracle(wh):
     assert np.array_equal(st.blend.out_last, st_o["out_last"])
     assert np.array_equal(st.blend.n_contrib, st_o["n_contrib"])
     assert np.abs(img.rgb - img_o["rgb"]).max() < 1e-5
+
+
+def test_depth_ties_follow_float64_then_index_order():
+    """Splats whose depths collide in float32 (but not float64), plus exact float64
+    duplicates: the instance order must still be np.lexsort((depth, tile))'s."""
+    from oracle import vegs_oracle as O
+    from paper_2504_13339_b200.constants import DEFAULT_SETTINGS as S
+
+    gs = scenes.random_gaussians(600, seed=11)
+    gs.log_scale[:] += 1.0
+    rng = np.random.default_rng(5)
+    # camera on the +z axis looking at the origin: depth = 3 - z
+    base = rng.uniform(-0.5, 0.5, size=(200, 1))
+    z = np.concatenate([base, base + 3e-9, base + 1.5e-8]).ravel()  # same float32 depth, distinct float64
+    gs.position[:, 2] = z[rng.permutation(600)]
+    gs.position[:50] = gs.position[50:100]  # exact duplicates (equal float64 depth): index order
+    tf = scenes.random_tf(11, 4)
+    cam = Camera(position=(0.0, 0.0, 3.0), target=(0.0, 0.0, 0.0), up=(0.0, 1.0, 0.0),
+                 fov_y=math.radians(50.0), width=64, height=64)
+    img, st = R.render_with_state(gs, tf, cam, (1.0, 1.0, 1.0), S, False, np.float32)
+    img_o, st_o = O.render_with_state(gs, tf, cam, (1.0, 1.0, 1.0), S, False, np.float32)
+    assert np.array_equal(st.blend.order, st_o["order"])
+    assert np.array_equal(st.blend.out_last, st_o["out_last"])
+    assert np.array_equal(st.blend.n_contrib, st_o["n_contrib"])
