@@ -45,6 +45,7 @@ sys.path.insert(0, str(ROOT))
 
 METRIC = "train steps/s at 1M Gaussians (config 2: 16 views/step @1024x1024)"
 UNIT = "steps/s"
+MAX_SM_MHZ = 1965.0  # B200 max SM clock; MEASURED_PEAKS.json sm_max_mhz overrides
 WORKLOAD = "c2"
 VIEWS_PER_STEP = 16
 
@@ -298,15 +299,32 @@ def run_b200(args) -> None:
         byts = [algorithmic_bytes(dom, nk, ni, 1024 * 1024) for nk, ni in rec["counts"]]
         avg_bytes = sum(byts) / len(byts)
         achieved = avg_bytes / (rec["avg_ms"] / 1000.0) / 1e9
-        traffic = None
-        prof = ROOT / "profiles" / "ncu_dram_bytes.json"
+        traffic, issue = None, None
+        prof = ROOT / "profiles" / "ncu_composite.json"
         if prof.exists():
-            traffic = json.loads(prof.read_text()).get(dom)
+            rec_ncu = json.loads(prof.read_text()).get(dom)
+            if rec_ncu:
+                traffic = rec_ncu["dram_bytes"]
+                # the bound that actually applies: warp-instruction issue (4 schedulers per SM)
+                props = torch.cuda.get_device_properties(dev)
+                mhz = MAX_SM_MHZ
+                try:
+                    mhz = float(json.loads((ROOT / "MEASURED_PEAKS.json").read_text())["sm_max_mhz"])
+                except Exception:
+                    pass
+                peak_issue = props.multi_processor_count * 4 * mhz * 1e6
+                achieved_issue = rec_ncu["warp_instructions"] / (rec["avg_ms"] / 1000.0)
+                issue = {"bound": "issue", "achieved": achieved_issue, "peak": peak_issue,
+                         "unit": "warp-instructions/s", "frac": achieved_issue / peak_issue,
+                         "warp_instructions_per_launch": rec_ncu["warp_instructions"],
+                         "peak_source": f"{props.multi_processor_count} SMs x 4 schedulers x {mhz:.0f} MHz",
+                         "source": "profiles/ncu_composite.json (instruction count) / live CUDA-event duration"}
         roof = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "peak_source": peak_kind,
                 "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
                 "algorithmic_bytes_per_launch": avg_bytes, "avg_launch_ms": rec["avg_ms"],
                 "share_of_step": rec["total_ms"] / ms / 1.0,
-                "note": "compositing is CUDA-core (FP32/FP64 + MUFU) bound, not HBM bound (SURVEY §8(d))"}
+                "note": "compositing is CUDA-core instruction-issue bound, not HBM bound (SURVEY §8(d)); "
+                        "see issue_roofline", "issue_roofline": issue}
     kernels = {k: {"avg_ms": v["avg_ms"], "launches": v["launches"], "share_of_step": v["total_ms"] / ms,
                    "avg_instances": sum(c[1] for c in v["counts"]) / len(v["counts"])}
                for k, v in ksum.items()}
