@@ -38,5 +38,23 @@ def main():
         print(f"slots {slots}: lower bound {lb:.0f}  launch order {nat:.0f} ({nat / lb:.3f})  heaviest-first {lpt:.0f} ({lpt / lb:.3f})")
 
 
+
+
+def warp_imbalance():
+    """Share of (warp, instance-slot) pairs a backward CTA spends above a warp's own last
+    contributor (the warp has nothing to do there but waits at the batch barriers)."""
+    gs, truth, tf, cams = scenes.config_scene("c2")
+    rz = Rasterizer()
+    params = torch.from_numpy(gs.pack()).cuda()
+    fr = rz.forward(params, len(gs), DeviceTF(tf), cams[0])
+    ts = fr.tile_start.cpu().numpy()
+    last = fr.out_last.view(1024, 1024).cpu().numpy()
+    blk = last.reshape(64, 2, 8, 64, 2, 8).transpose(0, 3, 1, 4, 2, 5).reshape(4096, 4, 64).max(2)
+    rel = np.where(blk >= 0, blk - ts[:, None] + 1, 0)
+    hi = rel.max(1, keepdims=True)
+    print("warp-last imbalance: idle share", float((hi - rel).sum() / max(4 * hi.sum(), 1)))
+
+
 if __name__ == "__main__":
     main()
+    warp_imbalance()
