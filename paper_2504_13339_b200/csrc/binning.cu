@@ -16,6 +16,8 @@
 // deterministic backward reduction relies on) is recomputed afterwards from the splat's
 // tile rectangle, so no per-instance indirection array is gathered.
 
+#include <stdlib.h>
+
 #include <cub/cub.cuh>
 
 #include "vegs_common.cuh"
@@ -181,6 +183,164 @@ __global__ void tile_weight_kernel(const int32_t *tile_start, const int32_t *til
     val[t] = t;
 }
 
+// ---- counting placement (no instance-level sort) ----------------------------------
+// The kept splats in depth order are cut into chunks of C.  (1) per chunk, per-tile
+// instance counts from a 2D difference array of the splats' tile rectangles; (2) those
+// counts, scanned tile-major over (tile, chunk), give every chunk its first output slot in
+// every tile; (3) one warp per chunk walks its splats in depth order and appends each
+// splat's id to each of its tiles.  Slots within a tile therefore follow (chunk, depth
+// rank) = depth rank order: exactly np.lexsort((depth, tile)), as the radix path.
+
+__global__ void chunk_count_kernel(const uint32_t *ids, const int4 *rect, int64_t n_kept, int C, int tiles_x,
+                                   int tiles_y, uint32_t *counts) {
+    extern __shared__ int diff[];  // (tiles_y + 1) x (tiles_x + 1)
+    const int c = blockIdx.x, W1 = tiles_x + 1, n_diff = (tiles_y + 1) * W1, n_tiles = tiles_x * tiles_y;
+    for (int i = threadIdx.x; i < n_diff; i += blockDim.x) diff[i] = 0;
+    __syncthreads();
+    const int64_t lo = (int64_t)c * C, hi = lo + C < n_kept ? lo + C : n_kept;
+    for (int64_t r = lo + threadIdx.x; r < hi; r += blockDim.x) {
+        const int4 q = __ldg(rect + ids[r]);
+        const int x0 = q.x / kTile, x1 = (q.y - 1) / kTile + 1, y0 = q.z / kTile, y1 = (q.w - 1) / kTile + 1;
+        atomicAdd(&diff[y0 * W1 + x0], 1);
+        atomicAdd(&diff[y0 * W1 + x1], -1);
+        atomicAdd(&diff[y1 * W1 + x0], -1);
+        atomicAdd(&diff[y1 * W1 + x1], 1);
+    }
+    __syncthreads();
+    for (int y = threadIdx.x; y < tiles_y; y += blockDim.x) {  // prefix along rows
+        int run = 0;
+        for (int x = 0; x < tiles_x; ++x) diff[y * W1 + x] = (run += diff[y * W1 + x]);
+    }
+    __syncthreads();
+    for (int x = threadIdx.x; x < tiles_x; x += blockDim.x) {  // prefix along columns
+        int run = 0;
+        for (int y = 0; y < tiles_y; ++y) counts[(size_t)c * n_tiles + y * tiles_x + x] = (uint32_t)(run += diff[y * W1 + x]);
+    }
+}
+
+// per (group of G chunks, tile): the group's instance count
+__global__ void chunk_group_sum_kernel(const uint32_t *counts, int n_chunks, int n_tiles, int G, uint32_t *gsum) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int n_groups = (n_chunks + G - 1) / G;
+    if (i >= (int64_t)n_groups * n_tiles) return;
+    const int grp = (int)(i / n_tiles), t = (int)(i - (int64_t)grp * n_tiles);
+    const int c0 = grp * G, c1 = (grp + 1) * G < n_chunks ? (grp + 1) * G : n_chunks;
+    uint32_t sum = 0;
+#pragma unroll 8
+    for (int c = c0; c < c1; ++c) sum += __ldg(counts + (size_t)c * n_tiles + t);
+    gsum[i] = sum;
+}
+
+// per tile: exclusive scan of the group counts (in place) and the tile total
+__global__ void tile_group_scan_kernel(uint32_t *gsum, int n_groups, int n_tiles, uint32_t *total) {
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= n_tiles) return;
+    uint32_t run = 0;
+    for (int g = 0; g < n_groups; ++g) {
+        const uint32_t v = gsum[(size_t)g * n_tiles + t];
+        gsum[(size_t)g * n_tiles + t] = run;
+        run += v;
+    }
+    total[t] = run;
+}
+
+// per (group, tile): counts -> first output slot of every chunk (in place); tile ranges
+__global__ void chunk_offsets_kernel(uint32_t *counts, const uint32_t *gbase, const int32_t *tile_start,
+                                     const uint32_t *total, int n_chunks, int n_tiles, int G, int32_t *tile_end) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int n_groups = (n_chunks + G - 1) / G;
+    if (i >= (int64_t)n_groups * n_tiles) return;
+    const int grp = (int)(i / n_tiles), t = (int)(i - (int64_t)grp * n_tiles);
+    if (grp == 0) tile_end[t] = tile_start[t] + (int32_t)total[t];
+    uint32_t run = (uint32_t)tile_start[t] + gbase[i];
+    const int c0 = grp * G, c1 = (grp + 1) * G < n_chunks ? (grp + 1) * G : n_chunks;
+    for (int cb = c0; cb < c1; cb += 8) {  // 8 loads in flight, then 8 stores
+        uint32_t v[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) v[q] = cb + q < c1 ? counts[(size_t)(cb + q) * n_tiles + t] : 0u;
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+            if (cb + q < c1) {
+                counts[(size_t)(cb + q) * n_tiles + t] = run;
+                run += v[q];
+            }
+    }
+}
+
+// one warp per chunk: splats in depth order, lanes over each splat's tiles (distinct tiles:
+// no conflicts inside a splat), per-tile cursors in SMEM
+__global__ void __launch_bounds__(32) place_kernel(const uint32_t *ids, const int4 *rect, int64_t n_kept, int C,
+                                                   int tiles_x, int n_tiles, const uint32_t *first,
+                                                   uint32_t *sorted_gauss) {
+    extern __shared__ uint32_t cursor[];
+    const int c = blockIdx.x, lane = threadIdx.x;
+    for (int t = lane; t < n_tiles; t += 32) cursor[t] = first[(size_t)c * n_tiles + t];
+    __syncwarp();
+    const int64_t lo = (int64_t)c * C, hi = lo + C < n_kept ? lo + C : n_kept;
+    // lane k holds splat r0 + k of the current group of 32; the next group's ids and rects
+    // are fetched while this one is placed
+    auto fetch = [&](int64_t r0, uint32_t &g, int4 &q) {
+        g = 0;
+        q = make_int4(0, 1, 0, 1);
+        if (r0 + lane < hi) {
+            g = ids[r0 + lane];
+            q = __ldg(rect + g);
+        }
+    };
+    uint32_t g_n;
+    int4 q_n;
+    fetch(lo, g_n, q_n);
+    for (int64_t r0 = lo; r0 < hi; r0 += 32) {
+        const uint32_t g = g_n;
+        const int4 q = q_n;
+        if (r0 + 32 < hi) fetch(r0 + 32, g_n, q_n);
+        const int x0 = q.x / kTile, y0 = q.z / kTile;
+        const int nx = (q.y - 1) / kTile - x0 + 1;
+        const int cnt = r0 + lane < hi ? nx * ((q.w - 1) / kTile - y0 + 1) : 0;
+        const float inx = 1.0f / (float)nx;
+        const int m = hi - r0 < 32 ? (int)(hi - r0) : 32;
+        for (int k = 0; k < m; ++k) {
+            const uint32_t gk = __shfl_sync(0xffffffffu, g, k);
+            const int x0k = __shfl_sync(0xffffffffu, x0, k), y0k = __shfl_sync(0xffffffffu, y0, k);
+            const int nxk = __shfl_sync(0xffffffffu, nx, k), ck = __shfl_sync(0xffffffffu, cnt, k);
+            const float ik = __shfl_sync(0xffffffffu, inx, k);
+            for (int j = lane; j < ck; j += 32) {
+                // j / nxk via the float reciprocal (exact for j < 2^20: the quotient is
+                // corrected by one step)
+                int dy = (int)((float)j * ik);
+                dy += (j - dy * nxk >= nxk) - (j - dy * nxk < 0);
+                const int dx = j - dy * nxk;
+                const int t = (y0k + dy) * tiles_x + (x0k + dx);
+                const uint32_t pos = cursor[t];
+                cursor[t] = pos + 1;
+                sorted_gauss[pos] = gk;
+            }
+            __syncwarp();
+        }
+    }
+}
+
+// API path only: the tile of each sorted instance (from the ranges), its kept index and
+// duplicate-order index
+__global__ void placed_extras_kernel(const uint32_t *sorted_gauss, const int4 *rect, const int64_t *offsets,
+                                     const int64_t *kept_idx, const int32_t *tile_end, int64_t n_inst, int n_tiles,
+                                     int tiles_x, uint32_t *inst_pid, int64_t *order) {
+    const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (s >= n_inst) return;
+    int lo = 0, hi = n_tiles - 1;  // first tile whose end exceeds s
+    while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (tile_end[mid] > s) hi = mid;
+        else lo = mid + 1;
+    }
+    const uint32_t gid = sorted_gauss[s];
+    if (inst_pid) {
+        const int ty = lo / tiles_x, tx = lo - ty * tiles_x;
+        inst_pid[s] = (uint32_t)dup_index(__ldg(offsets + gid), __ldg(rect + gid), tx, ty);
+    }
+    if (order) order[s] = kept_idx[gid];
+}
+
 static size_t align_up(size_t x) { return (x + 255) & ~size_t(255); }
 
 }  // namespace vegs
@@ -319,6 +479,107 @@ static int bin_sort_impl(const uint32_t *tiles, const uint64_t *depth_key, const
     return VEGS_OK;
 }
 
+// Counting-placement binning for up to kMaxPlaceTiles tiles (per-tile cursors and the
+// difference array live in SMEM); larger images, or VEGS_BIN_RADIX set in the environment
+// (tests), take the radix path above.
+constexpr int kMaxPlaceTiles = 12288;
+
+static int bin_place_impl(const uint64_t *depth_key, const int32_t *rect, const int64_t *offsets,
+                          const int64_t *kept_idx, int64_t n, int64_t n_kept, int64_t n_inst, int tiles_x,
+                          int tiles_y, uint32_t *sorted_gauss, uint32_t *inst_pid, int64_t *order,
+                          int32_t *tile_start, int32_t *tile_end, int32_t *tile_order, void *ws, size_t *ws_bytes,
+                          cudaStream_t s) {
+    const int n_tiles = tiles_x * tiles_y;
+#ifndef VEGS_PLACE_CHUNKS
+#define VEGS_PLACE_CHUNKS 4096
+#endif
+    constexpr int64_t kChunks = VEGS_PLACE_CHUNKS;  // target chunk count: warps for the placement
+    const int C = (int)(n_kept > kChunks * 128 ? (n_kept + kChunks - 1) / kChunks : 128);
+    const int n_chunks = n_kept > 0 ? (int)((n_kept + C - 1) / C) : 0;
+    const int G = 64, n_groups = (n_chunks + G - 1) / G;
+    size_t t_depth = 0, t_scan = 0, t_tiles = 0;
+    {
+        cub::DoubleBuffer<uint32_t> dk(nullptr, nullptr), dv(nullptr, nullptr);
+        VEGS_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, t_depth, dk, dv, (int64_t)n, 0, 32, s));
+        uint32_t *u = nullptr;
+        int32_t *v = nullptr;
+        VEGS_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, t_scan, u, v, n_tiles, s));
+        VEGS_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, t_tiles, u, u, v, v, n_tiles, 0, 16, s));
+    }
+    size_t t_max = t_depth > t_scan ? t_depth : t_scan;
+    t_max = t_max > t_tiles ? t_max : t_tiles;
+    const size_t b_n = align_up(sizeof(uint32_t) * (n + 1)), b_t = align_up(sizeof(uint32_t) * n_tiles);
+    const size_t b_cnt = align_up(sizeof(uint32_t) * (size_t)n_chunks * n_tiles);
+    const size_t b_grp = align_up(sizeof(uint32_t) * (size_t)n_groups * n_tiles);
+    const size_t need = 4 * b_n + b_cnt + b_grp + 4 * b_t + align_up(t_max);
+    if (!ws) {
+        *ws_bytes = need;
+        return VEGS_OK;
+    }
+    if (*ws_bytes < need) return VEGS_ERR_CAPACITY;
+    char *w = (char *)ws;
+    uint32_t *dk0 = (uint32_t *)w; w += b_n;
+    uint32_t *dk1 = (uint32_t *)w; w += b_n;
+    uint32_t *id0 = (uint32_t *)w; w += b_n;
+    uint32_t *id1 = (uint32_t *)w; w += b_n;
+    uint32_t *counts = (uint32_t *)w; w += b_cnt;
+    uint32_t *gsum = (uint32_t *)w; w += b_grp;
+    uint32_t *total = (uint32_t *)w; w += b_t;
+    uint32_t *tkey0 = (uint32_t *)w; w += b_t;
+    uint32_t *tkey1 = (uint32_t *)w; w += b_t;
+    int32_t *tval = (int32_t *)w; w += b_t;
+    void *tmp = w;
+    const size_t tb0 = align_up(t_max);
+
+    if (n_inst == 0) {
+        VEGS_CUDA(cudaMemsetAsync(tile_start, 0, sizeof(int32_t) * n_tiles, s));
+        VEGS_CUDA(cudaMemsetAsync(tile_end, 0, sizeof(int32_t) * n_tiles, s));
+    } else {
+        // 1. stable depth order of the kept splats (as in bin_sort_impl)
+        depth_key32_kernel<<<(int)((n + 255) / 256), 256, 0, s>>>(depth_key, n, dk0, id0);
+        VEGS_CHECK_LAUNCH();
+        cub::DoubleBuffer<uint32_t> dk(dk0, dk1), dv(id0, id1);
+        size_t tb = tb0;
+        VEGS_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tb, dk, dv, (int64_t)n, 0, 32, s));
+        depth_ties_kernel<<<(int)((n_kept + 255) / 256), 256, 0, s>>>(dk.Current(), depth_key, n_kept, dv.Current());
+        VEGS_CHECK_LAUNCH();
+        const uint32_t *ids = dv.Current();
+        // 2. per-chunk tile counts -> first slot of every chunk in every tile, tile ranges
+        const size_t diff_bytes = sizeof(int) * (size_t)(tiles_x + 1) * (tiles_y + 1);
+        chunk_count_kernel<<<n_chunks, 256, diff_bytes, s>>>(ids, (const int4 *)rect, n_kept, C, tiles_x, tiles_y,
+                                                             counts);
+        VEGS_CHECK_LAUNCH();
+        const int64_t ng = (int64_t)n_groups * n_tiles;
+        chunk_group_sum_kernel<<<(int)((ng + 255) / 256), 256, 0, s>>>(counts, n_chunks, n_tiles, G, gsum);
+        VEGS_CHECK_LAUNCH();
+        tile_group_scan_kernel<<<(n_tiles + 255) / 256, 256, 0, s>>>(gsum, n_groups, n_tiles, total);
+        VEGS_CHECK_LAUNCH();
+        tb = tb0;
+        VEGS_CUDA(cub::DeviceScan::ExclusiveSum(tmp, tb, total, tile_start, n_tiles, s));
+        chunk_offsets_kernel<<<(int)((ng + 255) / 256), 256, 0, s>>>(counts, gsum, tile_start, total, n_chunks,
+                                                                     n_tiles, G, tile_end);
+        VEGS_CHECK_LAUNCH();
+        // 3. placement, one warp per chunk
+        place_kernel<<<n_chunks, 32, sizeof(uint32_t) * n_tiles, s>>>(ids, (const int4 *)rect, n_kept, C, tiles_x,
+                                                                     n_tiles, counts, sorted_gauss);
+        VEGS_CHECK_LAUNCH();
+        if (inst_pid || order) {
+            placed_extras_kernel<<<(int)((n_inst + 255) / 256), 256, 0, s>>>(
+                sorted_gauss, (const int4 *)rect, offsets, kept_idx, tile_end, n_inst, n_tiles, tiles_x, inst_pid,
+                order);
+            VEGS_CHECK_LAUNCH();
+        }
+    }
+    // 4. optional launch order for the compositing kernels: heaviest tiles first
+    if (tile_order) {
+        tile_weight_kernel<<<(n_tiles + 255) / 256, 256, 0, s>>>(tile_start, tile_end, n_tiles, tkey0, tval);
+        VEGS_CHECK_LAUNCH();
+        size_t tb = tb0;
+        VEGS_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tb, tkey0, tkey1, tval, tile_order, n_tiles, 0, 16, s));
+    }
+    return VEGS_OK;
+}
+
 extern "C" int vegs_bin_sort(const uint32_t *tiles, const uint64_t *depth_key, const int32_t *rect,
                              const int64_t *offsets, const int64_t *kept_idx, int64_t n, int64_t n_kept,
                              int64_t n_inst, int32_t width, int32_t height, int32_t tile_size,
@@ -332,6 +593,9 @@ extern "C" int vegs_bin_sort(const uint32_t *tiles, const uint64_t *depth_key, c
     const int tiles_x = (width + kTile - 1) / kTile, tiles_y = (height + kTile - 1) / kTile;
     const int n_tiles = tiles_x * tiles_y;
     cudaStream_t s = (cudaStream_t)stream;
+    if ((tiles_x + 1) * (tiles_y + 1) <= kMaxPlaceTiles && !getenv("VEGS_BIN_RADIX"))
+        return bin_place_impl(depth_key, rect, offsets, kept_idx, n, n_kept, n_inst, tiles_x, tiles_y, sorted_gauss,
+                              inst_pid, order, tile_start, tile_end, tile_order, ws, ws_bytes, s);
     if (n_tiles <= 65536)
         return bin_sort_impl<uint16_t>(tiles, depth_key, rect, offsets, kept_idx, n, n_kept, n_inst, tiles_x,
                                        n_tiles, sorted_gauss, inst_pid, order, tile_start, tile_end, tile_order, ws,

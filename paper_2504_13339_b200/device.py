@@ -19,6 +19,7 @@ from __future__ import annotations
 
 import ctypes
 import math
+import os
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -37,10 +38,10 @@ LAUNCHES = {
     "vegs_preprocess_forward": 1,
     "vegs_splat_table_from_arrays": 1,
     "vegs_bin_count": 4,          # pack, CUB scan (init + sweep), unpack
-    "vegs_bin_sort": 19,          # coarse keys, CUB depth sort (hist + scan + 4 onesweep), ties, depth counts, scan (2),
-                                  # duplicate,
-                                  # CUB key sort (hist + scan + 2 onesweep), finalize, tile weights +
-                                  # single-tile CUB sort (heaviest-first tile order)
+    "vegs_bin_sort": 18,          # counting placement: coarse keys, CUB depth sort (hist + scan + 4 onesweep), ties,
+                                  # chunk counts, group sums, group scan, CUB scan (2), chunk offsets, placement,
+                                  # tile weights + single-tile CUB sort (heaviest-first tile order); +1 (order /
+                                  # inst_pid) on the API path.  Radix path (> 12288 tiles): 19.
     "vegs_composite_forward": 1,
     "vegs_composite_backward": 1,
     "vegs_preprocess_backward": 2,  # row reduction + chain
@@ -292,6 +293,10 @@ class Rasterizer:
         wsz = _lib.size_query("vegs_bin_sort", *args, tail=(s,))
         ws = A.get("ws_sort", wsz, torch.uint8)
         self._run("vegs_bin_sort", *args, _p(ws), ctypes.byref(ctypes.c_size_t(wsz)), s)
+        if (tiles_x + 1) * ((height + TILE - 1) // TILE + 1) > 12288 or os.environ.get("VEGS_BIN_RADIX"):
+            self.launches += 1  # radix path
+        elif want_order:
+            self.launches += 1  # order / inst_pid for the reference-shaped API
         hw = width * height
         out_img = A.get("out_img", hw * self.n_ch, self.real)
         out_t = A.get("out_t", hw, self.real)

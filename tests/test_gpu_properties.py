@@ -175,3 +175,28 @@ def test_depth_ties_follow_float64_then_index_order():
     assert np.array_equal(st.blend.order, st_o["order"])
     assert np.array_equal(st.blend.out_last, st_o["out_last"])
     assert np.array_equal(st.blend.n_contrib, st_o["n_contrib"])
+
+
+@pytest.mark.parametrize("wh", [(512, 512), (1920, 1080)])
+def test_counting_placement_equals_radix_binning(wh, monkeypatch):
+    """The counting-placement binning and the radix-sort binning produce the same instance
+    order, ranges and images (both equal np.lexsort((depth, tile)))."""
+    from paper_2504_13339_b200.device import DeviceTF, Rasterizer
+
+    gs = scenes.random_gaussians(100_000, seed=21)
+    tf = scenes.random_tf(21, 4)
+    cam = scenes.orbit_cameras(1, 22, wh[0], wh[1])[0]
+    params = torch.from_numpy(gs.pack()).cuda()
+    dtf = DeviceTF(tf)
+    out = []
+    for radix in (False, True):
+        if radix:
+            monkeypatch.setenv("VEGS_BIN_RADIX", "1")
+        rz = Rasterizer(pooled=False)
+        fr = rz.forward(params, len(gs), dtf, cam, want_order=True)
+        out.append({k: getattr(fr, k).cpu().clone() for k in
+                    ("sorted_gauss", "inst_pid", "order", "tile_start", "tile_end", "out_last", "out_img", "out_t")})
+    a, b = out
+    assert a["sorted_gauss"].numel() > 1000
+    for k in a:
+        assert torch.equal(a[k], b[k]), k
