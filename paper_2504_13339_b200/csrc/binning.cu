@@ -267,15 +267,20 @@ __global__ void chunk_offsets_kernel(uint32_t *counts, const uint32_t *gbase, co
     }
 }
 
-// one warp per chunk: splats in depth order, lanes over each splat's tiles (distinct tiles:
-// no conflicts inside a splat), per-tile cursors in SMEM
-__global__ void __launch_bounds__(32) place_kernel(const uint32_t *ids, const int4 *rect, int64_t n_kept, int C,
-                                                   int tiles_x, int n_tiles, const uint32_t *first,
-                                                   uint32_t *sorted_gauss) {
+// One CTA per chunk, one warp per horizontal band of tile rows (kBands bands): each warp
+// walks the chunk's splats in depth order and appends, for the part of each splat's tile
+// rectangle inside its band, the splat id to each tile (distinct tiles inside a splat: no
+// conflicts); per-tile cursors in SMEM.  The bands multiply the warps in flight.
+constexpr int kBands = 4;
+__global__ void __launch_bounds__(32 * kBands) place_kernel(const uint32_t *ids, const int4 *rect, int64_t n_kept,
+                                                            int C, int tiles_x, int tiles_y, const uint32_t *first,
+                                                            uint32_t *sorted_gauss) {
     extern __shared__ uint32_t cursor[];
-    const int c = blockIdx.x, lane = threadIdx.x;
-    for (int t = lane; t < n_tiles; t += 32) cursor[t] = first[(size_t)c * n_tiles + t];
-    __syncwarp();
+    const int n_tiles = tiles_x * tiles_y;
+    const int c = blockIdx.x, lane = threadIdx.x & 31, band = threadIdx.x >> 5;
+    for (int t = threadIdx.x; t < n_tiles; t += blockDim.x) cursor[t] = first[(size_t)c * n_tiles + t];
+    __syncthreads();
+    const int band_lo = band * tiles_y / kBands, band_hi = (band + 1) * tiles_y / kBands - 1;  // tile rows
     const int64_t lo = (int64_t)c * C, hi = lo + C < n_kept ? lo + C : n_kept;
     // lane k holds splat r0 + k of the current group of 32; the next group's ids and rects
     // are fetched while this one is placed
@@ -294,14 +299,16 @@ __global__ void __launch_bounds__(32) place_kernel(const uint32_t *ids, const in
         const uint32_t g = g_n;
         const int4 q = q_n;
         if (r0 + 32 < hi) fetch(r0 + 32, g_n, q_n);
-        const int x0 = q.x / kTile, y0 = q.z / kTile;
-        const int nx = (q.y - 1) / kTile - x0 + 1;
-        const int cnt = r0 + lane < hi ? nx * ((q.w - 1) / kTile - y0 + 1) : 0;
+        const int x0 = q.x / kTile, nx = (q.y - 1) / kTile - x0 + 1;
+        const int ys = max(q.z / kTile, band_lo), ye = min((q.w - 1) / kTile, band_hi);
+        const int cnt = r0 + lane < hi && ys <= ye ? nx * (ye - ys + 1) : 0;
         const float inx = 1.0f / (float)nx;
-        const int m = hi - r0 < 32 ? (int)(hi - r0) : 32;
-        for (int k = 0; k < m; ++k) {
+        unsigned todo = __ballot_sync(0xffffffffu, cnt > 0);  // splats of the group touching this band
+        while (todo) {
+            const int k = __ffs(todo) - 1;
+            todo &= todo - 1;
             const uint32_t gk = __shfl_sync(0xffffffffu, g, k);
-            const int x0k = __shfl_sync(0xffffffffu, x0, k), y0k = __shfl_sync(0xffffffffu, y0, k);
+            const int x0k = __shfl_sync(0xffffffffu, x0, k), ysk = __shfl_sync(0xffffffffu, ys, k);
             const int nxk = __shfl_sync(0xffffffffu, nx, k), ck = __shfl_sync(0xffffffffu, cnt, k);
             const float ik = __shfl_sync(0xffffffffu, inx, k);
             for (int j = lane; j < ck; j += 32) {
@@ -310,7 +317,7 @@ __global__ void __launch_bounds__(32) place_kernel(const uint32_t *ids, const in
                 int dy = (int)((float)j * ik);
                 dy += (j - dy * nxk >= nxk) - (j - dy * nxk < 0);
                 const int dx = j - dy * nxk;
-                const int t = (y0k + dy) * tiles_x + (x0k + dx);
+                const int t = (ysk + dy) * tiles_x + (x0k + dx);
                 const uint32_t pos = cursor[t];
                 cursor[t] = pos + 1;
                 sorted_gauss[pos] = gk;
@@ -491,7 +498,7 @@ static int bin_place_impl(const uint64_t *depth_key, const int32_t *rect, const 
                           cudaStream_t s) {
     const int n_tiles = tiles_x * tiles_y;
 #ifndef VEGS_PLACE_CHUNKS
-#define VEGS_PLACE_CHUNKS 4096
+#define VEGS_PLACE_CHUNKS 2048
 #endif
     constexpr int64_t kChunks = VEGS_PLACE_CHUNKS;  // target chunk count: warps for the placement
     const int C = (int)(n_kept > kChunks * 128 ? (n_kept + kChunks - 1) / kChunks : 128);
@@ -560,8 +567,8 @@ static int bin_place_impl(const uint64_t *depth_key, const int32_t *rect, const 
                                                                      n_tiles, G, tile_end);
         VEGS_CHECK_LAUNCH();
         // 3. placement, one warp per chunk
-        place_kernel<<<n_chunks, 32, sizeof(uint32_t) * n_tiles, s>>>(ids, (const int4 *)rect, n_kept, C, tiles_x,
-                                                                     n_tiles, counts, sorted_gauss);
+        place_kernel<<<n_chunks, 32 * kBands, sizeof(uint32_t) * n_tiles, s>>>(ids, (const int4 *)rect, n_kept, C,
+                                                                              tiles_x, tiles_y, counts, sorted_gauss);
         VEGS_CHECK_LAUNCH();
         if (inst_pid || order) {
             placed_extras_kernel<<<(int)((n_inst + 255) / 256), 256, 0, s>>>(

@@ -200,3 +200,31 @@ def test_counting_placement_equals_radix_binning(wh, monkeypatch):
     assert a["sorted_gauss"].numel() > 1000
     for k in a:
         assert torch.equal(a[k], b[k]), k
+
+
+def test_two_pixel_backward_matches_four_pixel_backward(monkeypatch):
+    """The two-pixel-per-lane backward (kept behind VEGS_BWD2) and the default four-pixel
+    one reduce the same per-instance sums in a different order: equal to float32 rounding,
+    and both equal to the oracle."""
+    from oracle import vegs_oracle as O
+    from paper_2504_13339_b200.constants import DEFAULT_SETTINGS as S
+
+    gs = scenes.random_gaussians(20_000, seed=31)
+    tf = scenes.random_tf(31, 4)
+    cam = scenes.orbit_cameras(1, 32, 256, 192)[0]
+    d_rgb = np.random.default_rng(33).uniform(-1, 1, size=(192, 256, 3))
+    img_o, st_o = O.render_with_state(gs, tf, cam, (1.0, 1.0, 1.0), S, False, np.float32)
+    g_o = O.rasterize_backward(st_o, d_rgb)
+    out = []
+    for two in (False, True):
+        if two:
+            monkeypatch.setenv("VEGS_BWD2", "1")
+        img, st = R.render_with_state(gs, tf, cam, (1.0, 1.0, 1.0), S, False, np.float32)
+        g = R.rasterize_backward(st, R.ImageGradients(rgb=d_rgb))
+        out.append(g)
+        for k in O.GRAD_CLASSES:
+            ref = g_o[k]
+            assert np.abs(getattr(g, k) - ref).max() <= 1e-4 * max(np.abs(ref).max(), 1e-300), (two, k)
+    for k in O.GRAD_CLASSES:
+        a, b = getattr(out[0], k), getattr(out[1], k)
+        assert np.abs(a - b).max() <= 1e-5 * max(np.abs(a).max(), 1e-300), k
