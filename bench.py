@@ -286,6 +286,9 @@ def run_b200(args) -> None:
     e2e = {"value": 1000.0 / e2e_ms, "unit": UNIT, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": 8,
            "ms_per_step": e2e_ms}
 
+    # the config-3 sweep has its own barrier / max-over-ranks: every rank takes part
+    sweep = None if args.no_sweep else run_sweep(args, dev, rank, world)
+
     if rank != 0:
         dist.destroy_process_group() if world > 1 else None
         return
@@ -328,8 +331,6 @@ def run_b200(args) -> None:
     kernels = {k: {"avg_ms": v["avg_ms"], "launches": v["launches"], "share_of_step": v["total_ms"] / ms,
                    "avg_instances": sum(c[1] for c in v["counts"]) / len(v["counts"])}
                for k, v in ksum.items()}
-
-    sweep = None if args.no_sweep else run_sweep(args, dev, rank, world)
 
     cpu = None
     if world == 1 and not args.no_cpu_baseline:

@@ -483,3 +483,42 @@ def test_trainer_aux_step_matches_reference_iteration():
         step_ref = d["out_" + k] - getattr(learned, k)
         step_gpu = getattr(out, k) - getattr(learned, k)
         assert G.norm_rel(step_gpu, step_ref) <= 1e-3, k
+
+
+def test_trainer_nccl_group_of_one():
+    """The NCCL plumbing the sharded step uses (process group on cuda:0, the trainer's
+    gradient all-reduce through it, max-over-ranks timing): a world of one rank gives the
+    same step as no group at all."""
+    import socket
+
+    import torch.distributed as dist
+
+    from paper_2504_13339_b200 import scenes
+    from paper_2504_13339_b200.device import DeviceTF
+    from paper_2504_13339_b200.parallel import allreduce_gradients
+    from paper_2504_13339_b200.train import Trainer, TrainConfig, View
+
+    d = G.load("train_step")
+    learned = scenes.random_gaussians(2000, seed=0)
+    dtf = DeviceTF(scenes.random_tf(2, 4))
+    cams = scenes.orbit_cameras(2, 3, 64, 64)
+    views = [View(c, dtf, torch.from_numpy(d[f"target{i}"]).cuda()) for i, c in enumerate(cams)]
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    store = dist.TCPStore("127.0.0.1", port, 1, True)
+    dist.init_process_group("nccl", store=store, rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        t = torch.ones(8, dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dist.barrier()
+        assert torch.equal(t, torch.ones_like(t))
+        g = torch.arange(6, dtype=torch.float64, device="cuda")
+        assert torch.equal(allreduce_gradients(g.clone(), dist.group.WORLD), g)
+        a = Trainer(learned, TrainConfig(iterations=100), group=dist.group.WORLD)
+        la = float(a.step(views, iteration=1).item())
+    finally:
+        dist.destroy_process_group()
+    b = Trainer(learned, TrainConfig(iterations=100))
+    lb = float(b.step(views, iteration=1).item())
+    assert la == lb and torch.equal(a.params, b.params)
