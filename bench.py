@@ -61,6 +61,7 @@ def parse():
     ap.add_argument("--cpu-budget-s", type=float, default=60.0)
     ap.add_argument("--no-sweep", action="store_true", help="skip the config-3 TF-sweep render measurement")
     ap.add_argument("--sweep-frames", type=int, default=2)
+    ap.add_argument("--lanes", type=int, default=3, help="CUDA-stream lanes of the view pipeline")
     ap.add_argument("--backend", choices=("nccl", "gloo"), default="nccl",
                     help="gradient all-reduce backend for N>1 (gloo: host-side plumbing check only)")
     return ap.parse_args()
@@ -200,7 +201,7 @@ def run_b200(args) -> None:
     torch.cuda.synchronize()
 
     group = dist.group.WORLD if world > 1 else None
-    trainer = Trainer(learned, TrainConfig(iterations=30000), group=group)
+    trainer = Trainer(learned, TrainConfig(iterations=30000), group=group, lanes=args.lanes)
     views = [View(cams[i], dtf, targets[j]) for j, i in enumerate(mine)]
 
     def barrier():

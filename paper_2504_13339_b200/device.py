@@ -410,7 +410,7 @@ class RenderPipeline:
     count, so the small per-view kernels overlap the previous view's compositing.
     Output frames are only valid until the lane that produced them is reused."""
 
-    def __init__(self, settings: RasterSettings = DEFAULT_SETTINGS, n_channels: int = 3, lanes: int = 2):
+    def __init__(self, settings: RasterSettings = DEFAULT_SETTINGS, n_channels: int = 3, lanes: int = 3):
         dev = require_cuda()
         main = torch.cuda.current_stream()
         self.lanes = [(main if i == 0 else torch.cuda.Stream(dev), Rasterizer(settings, n_channels, pooled=True))

@@ -194,7 +194,7 @@ class Trainer:
 
     def __init__(self, gs: GaussianSet, config: TrainConfig, settings: RasterSettings = DEFAULT_SETTINGS,
                  background=(1.0, 1.0, 1.0), l1_weight: float | None = None, group=None, with_aux: bool = False,
-                 lanes: int = 2):
+                 lanes: int = 3):
         self.device = require_cuda()
         self.n = len(gs)
         self.config = config
