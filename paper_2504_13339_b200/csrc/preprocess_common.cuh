@@ -1,0 +1,250 @@
+// Per-Gaussian device helpers shared by the preprocess (forward, -fmad=false) and the
+// preprocess backward (FMA contraction allowed) translation units: TF lookup, shading,
+// projection, record layout.  Header-only: every includer compiles its own copy with
+// its own floating-point contraction setting.
+#pragma once
+
+#include <math.h>
+
+#include "vegs_common.cuh"
+
+namespace vegs {
+namespace {  // internal linkage: each translation unit compiles its own copy
+
+
+// ---------------------------------------------------------------------------------
+// Transfer function: np.interp semantics (numpy compiled_base.c arr_interp) and the
+// half-open-segment slope of transfer.py:106-127.
+
+__device__ __forceinline__ int knot_segment(const double *ts, int k, double x) {
+    // largest j with ts[j] <= x (x inside [ts[0], ts[k-1]])
+    int lo = 0, hi = k;
+    while (hi - lo > 1) {
+        const int mid = (lo + hi) >> 1;
+        if (ts[mid] <= x) lo = mid; else hi = mid;
+    }
+    return lo;
+}
+
+__device__ __forceinline__ double clip01(double v) { return v < 0.0 ? 0.0 : (v > 1.0 ? 1.0 : v); }
+
+__device__ double tf_interp(const double *ts, const double *vals, int k, double x) {
+    if (x != x) return x;
+    if (x < ts[0]) return vals[0];
+    if (x > ts[k - 1]) return vals[k - 1];
+    const int j = knot_segment(ts, k, x);
+    if (j == k - 1 || ts[j] == x) return vals[j];
+    const double slope = (vals[j + 1] - vals[j]) / (ts[j + 1] - ts[j]);
+    return slope * (x - ts[j]) + vals[j];
+}
+
+__device__ double tf_slope(const double *ts, const double *vals, int k, double x) {
+    int j = (x < ts[0]) ? -1 : knot_segment(ts, k, x);
+    j = j < 0 ? 0 : (j > k - 2 ? k - 2 : j);
+    return (vals[j + 1] - vals[j]) / (ts[j + 1] - ts[j]);
+}
+
+__device__ __forceinline__ double sigmoid(double x) { return 1.0 / (1.0 + exp(-x)); }
+
+// TF tables staged in shared memory: [ts_op | op | ts_col | r | g | b]
+struct TFTable {
+    const double *ts_op, *op, *ts_col, *rgb[3];
+    int k_op, k_col;
+};
+
+__device__ TFTable stage_tf(const VegsTF &tf, double *smem) {
+    const int total = 2 * tf.n_opacity + 4 * tf.n_color;
+    for (int i = threadIdx.x; i < total; i += blockDim.x) smem[i] = tf.blob[i];
+    __syncthreads();
+    TFTable t;
+    t.k_op = tf.n_opacity;
+    t.k_col = tf.n_color;
+    t.ts_op = smem;
+    t.op = smem + t.k_op;
+    t.ts_col = smem + 2 * t.k_op;
+    t.rgb[0] = t.ts_col + t.k_col;
+    t.rgb[1] = t.rgb[0] + t.k_col;
+    t.rgb[2] = t.rgb[1] + t.k_col;
+    return t;
+}
+
+// ---------------------------------------------------------------------------------
+// Forward per-Gaussian state, recomputed by the backward from the raw parameters.
+
+struct Shaded {
+    double v, w, op, cmap[3], alpha_base, light[3], dist, n_hat[3], n_norm, ndotl, ka, kd, ks,
+        beta, spec, color[3];
+    bool visible;
+};
+
+struct Projected {
+    double t[3], txc, tyc, px, py, q_hat[4], q_norm, R[3][3], scale[3], sigma[3][3], M[2][3],
+        a, b, c, det, lam, conic[3], radius;
+    bool xhit, yhit, keep;
+    int x0, x1, y0, y1;
+};
+
+__device__ void shade_one(const ParamView &P, int64_t g, const TFTable &tf, const VegsCamera &cam,
+                          const VegsSettings &st, Shaded &s) {
+    s.v = sigmoid(P.raw_value[g]);
+    s.w = sigmoid(P.raw_weight[g]);
+    const double vc = clip01(s.v);
+    s.op = tf_interp(tf.ts_op, tf.op, tf.k_op, vc);
+    for (int c = 0; c < 3; ++c) s.cmap[c] = tf_interp(tf.ts_col, tf.rgb[c], tf.k_col, vc);
+    s.alpha_base = s.op * s.w;
+    double d[3], nn2 = 0.0, dd2 = 0.0;
+    for (int k = 0; k < 3; ++k) {
+        d[k] = cam.position[k] - P.pos[3 * g + k];
+        dd2 = dd2 + d[k] * d[k];
+    }
+    s.dist = sqrt(dd2);
+    for (int k = 0; k < 3; ++k) s.light[k] = d[k] / s.dist;
+    for (int k = 0; k < 3; ++k) nn2 = nn2 + P.normal[3 * g + k] * P.normal[3 * g + k];
+    s.n_norm = sqrt(nn2);
+    const double nd = fmax(s.n_norm, 1e-30);
+    s.ndotl = 0.0;
+    for (int k = 0; k < 3; ++k) {
+        s.n_hat[k] = P.normal[3 * g + k] / nd;
+        s.ndotl = s.ndotl + s.n_hat[k] * s.light[k];
+    }
+    const double sa = fabs(s.ndotl);
+    s.ka = sigmoid(P.raw_ka[g]);
+    s.kd = sigmoid(P.raw_kd[g]);
+    s.ks = sigmoid(P.raw_ks[g]);
+    s.beta = fmin(fmax(exp(P.raw_beta[g]), kBetaMin), kBetaMax);
+    s.spec = sa > 0.0 ? pow(fmax(sa, 1e-300), s.beta) : 0.0;
+    const double diffuse = s.ka + s.kd * sa;
+    const double specular = s.ks * s.spec;
+    for (int c = 0; c < 3; ++c) s.color[c] = diffuse * s.cmap[c] + specular;
+    s.visible = s.alpha_base >= st.cull_alpha;
+}
+
+template <bool kRect = true>
+__device__ void project_one(const ParamView &P, int64_t g, double alpha_base, const VegsCamera &cam,
+                            const VegsSettings &st, Projected &p) {
+    const double *W = cam.rot;
+    double d[3];
+    for (int k = 0; k < 3; ++k) d[k] = P.pos[3 * g + k] - cam.position[k];
+    for (int i = 0; i < 3; ++i) p.t[i] = d[0] * W[3 * i] + d[1] * W[3 * i + 1] + d[2] * W[3 * i + 2];
+    const double tz = p.t[2];
+    const bool front = tz > cam.near_z;
+    const double lim_x = st.frustum_limit * cam.tan_x;
+    const double lim_y = st.frustum_limit * cam.tan_y;
+    const double zs = front ? tz : 1.0;
+    const double txz = p.t[0] / zs, tyz = p.t[1] / zs;
+    p.xhit = fabs(txz) > lim_x;
+    p.yhit = fabs(tyz) > lim_y;
+    p.txc = fmin(fmax(txz, -lim_x), lim_x) * tz;
+    p.tyc = fmin(fmax(tyz, -lim_y), lim_y) * tz;
+    const double f = cam.focal;
+    p.px = 0.5 * (double)cam.width + f * txz;
+    p.py = 0.5 * (double)cam.height - f * tyz;
+
+    double q[4], qq = 0.0;
+    for (int k = 0; k < 4; ++k) {
+        q[k] = P.rot[4 * g + k];
+        qq = qq + q[k] * q[k];
+    }
+    p.q_norm = sqrt(qq);
+    const double qd = fmax(p.q_norm, 1e-30);
+    for (int k = 0; k < 4; ++k) p.q_hat[k] = q[k] / qd;
+    const double w = p.q_hat[0], x = p.q_hat[1], y = p.q_hat[2], z = p.q_hat[3];
+    p.R[0][0] = 1 - 2 * (y * y + z * z);
+    p.R[0][1] = 2 * (x * y - w * z);
+    p.R[0][2] = 2 * (x * z + w * y);
+    p.R[1][0] = 2 * (x * y + w * z);
+    p.R[1][1] = 1 - 2 * (x * x + z * z);
+    p.R[1][2] = 2 * (y * z - w * x);
+    p.R[2][0] = 2 * (x * z - w * y);
+    p.R[2][1] = 2 * (y * z + w * x);
+    p.R[2][2] = 1 - 2 * (x * x + y * y);
+    double s2[3];
+    for (int k = 0; k < 3; ++k) {
+        p.scale[k] = exp(P.log_scale[3 * g + k]);
+        s2[k] = p.scale[k] * p.scale[k];
+    }
+    for (int i = 0; i < 3; ++i)
+        for (int j = 0; j < 3; ++j) {
+            double acc = 0.0;
+            for (int k = 0; k < 3; ++k) acc = acc + (p.R[i][k] * s2[k]) * p.R[j][k];
+            p.sigma[i][j] = acc;
+        }
+    const double iz = 1.0 / zs, iz2 = iz * iz;
+    const double j00 = f * iz, j02 = -f * p.txc * iz2;
+    const double j11 = -f * iz, j12 = f * p.tyc * iz2;
+    for (int k = 0; k < 3; ++k) {
+        p.M[0][k] = j00 * W[k] + j02 * W[6 + k];
+        p.M[1][k] = j11 * W[3 + k] + j12 * W[6 + k];
+    }
+    double A[2][3];
+    for (int i = 0; i < 2; ++i)
+        for (int k = 0; k < 3; ++k)
+            A[i][k] = (p.M[i][0] * p.sigma[0][k] + p.M[i][1] * p.sigma[1][k]) + p.M[i][2] * p.sigma[2][k];
+    double cov[2][2];
+    for (int i = 0; i < 2; ++i)
+        for (int l = 0; l < 2; ++l)
+            cov[i][l] = (A[i][0] * p.M[l][0] + A[i][1] * p.M[l][1]) + A[i][2] * p.M[l][2];
+    p.a = cov[0][0] + st.dilation;
+    p.b = cov[0][1];
+    p.c = cov[1][1] + st.dilation;
+    p.det = p.a * p.c - p.b * p.b;
+    const double mid = 0.5 * (p.a + p.c);
+    p.lam = mid + sqrt(fmax(mid * mid - p.det, 0.0));
+    p.radius = st.radius_sigma * sqrt(fmax(p.lam, 0.0));
+    const double inv_det = p.det > 0 ? 1.0 / p.det : 0.0;
+    p.conic[0] = p.c * inv_det;
+    p.conic[1] = -p.b * inv_det;
+    p.conic[2] = p.a * inv_det;
+    if constexpr (!kRect) {  // the backward only needs the projection, not the rect
+        p.keep = front && (p.det > 0);
+        return;
+    }
+    const double ratio = fmax(alpha_base, st.alpha_skip) / st.alpha_skip;
+    const double rc = sqrt(fmax(p.lam, 0.0) * 2.0 * log(ratio)) + st.rect_margin_px;
+    const double Wd = (double)cam.width, Hd = (double)cam.height;
+    const double fx0 = fmin(fmax(ceil(p.px - rc - 0.5), 0.0), Wd);
+    const double fx1 = fmin(fmax(floor(p.px + rc - 0.5) + 1.0, 0.0), Wd);
+    const double fy0 = fmin(fmax(ceil(p.py - rc - 0.5), 0.0), Hd);
+    const double fy1 = fmin(fmax(floor(p.py + rc - 0.5) + 1.0, 0.0), Hd);
+    const bool finite = isfinite(p.px) && isfinite(p.py);
+    p.x0 = finite ? (int)fx0 : 0;
+    p.x1 = finite ? (int)fx1 : 0;
+    p.y0 = finite ? (int)fy0 : 0;
+    p.y1 = finite ? (int)fy1 : 0;
+    p.keep = front && (p.det > 0) && (p.x1 > p.x0) && (p.y1 > p.y0) && finite;
+}
+
+// Total order on float64 -> uint64 (negative values flipped), so a radix sort of the
+// keys is a sort of the depths; culled splats carry ~0.
+__device__ __forceinline__ uint64_t depth_order_key(double d) {
+    const uint64_t b = (uint64_t)__double_as_longlong(d);
+    return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
+}
+
+template <typename Real>
+__device__ void write_record(Real *r, double px, double py, const double *conic, double alpha_base,
+                             double alpha_skip) {
+    const double pmin = log(alpha_skip / fmax(alpha_base, alpha_skip * 1e-6));  // pipeline.py:207
+    r[0] = (Real)px;
+    r[1] = (Real)py;
+    r[2] = (Real)conic[0];
+    r[3] = (Real)conic[1];
+    r[4] = (Real)conic[2];
+    r[5] = (Real)alpha_base;
+    r[6] = (Real)pmin;
+}
+
+// ---------------------------------------------------------------------------------
+
+
+static inline size_t tf_smem_bytes(const VegsTF &tf) {
+    return sizeof(double) * (size_t)(2 * tf.n_opacity + 4 * tf.n_color);
+}
+
+static inline bool tf_ok(const VegsTF *tf) {
+    return tf && tf->blob && tf->n_opacity >= 2 && tf->n_color >= 2 && tf->n_opacity <= VEGS_MAX_KNOTS &&
+           tf->n_color <= VEGS_MAX_KNOTS;
+}
+
+}  // namespace
+}  // namespace vegs
