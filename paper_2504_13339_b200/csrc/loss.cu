@@ -37,8 +37,11 @@ __device__ __forceinline__ float block_sum_f(float v, float *red) {
 __global__ void __launch_bounds__(256) ssim_fwd_kernel(const float *__restrict__ x, const float *__restrict__ y,
                                                        int H, int W, int xs, Taps taps, float c1, float c2,
                                                        float coeff, float *__restrict__ maps, double *sums) {
-    __shared__ float sx[kIn][kIn + 1], sy[kIn][kIn + 1];
-    __shared__ float hs[5][kIn][kLT + 1];
+    // (x, y) pairs interleaved so the two blurs of x and y (and of x^2, y^2) run as packed
+    // FFMA2 on one LDS.64 per tap; x*y is blurred alone
+    __shared__ float2 sxy[kIn][kIn + 1];
+    __shared__ float2 h01[kIn][kLT + 1], h23[kIn][kLT + 1];
+    __shared__ float h4[kIn][kLT + 1];
     __shared__ float red[8];
     const int Hv = H - 2 * kHalf, Wv = W - 2 * kHalf;
     const int u0 = blockIdx.y * kLT, v0 = blockIdx.x * kLT;  // valid-output tile origin
@@ -50,44 +53,44 @@ __global__ void __launch_bounds__(256) ssim_fwd_kernel(const float *__restrict__
             const int r = i / kIn, q = i - r * kIn;
             const int gy = u0 + r, gx = v0 + q;
             const bool ok = gy < H && gx < W;
-            sx[r][q] = ok ? x[((int64_t)gy * W + gx) * xs + c] : 0.f;
-            sy[r][q] = ok ? y[((int64_t)gy * W + gx) * 3 + c] : 0.f;
+            sxy[r][q] = ok ? make_float2(x[((int64_t)gy * W + gx) * xs + c], y[((int64_t)gy * W + gx) * 3 + c])
+                           : make_float2(0.f, 0.f);
         }
         __syncthreads();
         for (int i = threadIdx.x; i < kIn * kLT; i += blockDim.x) {
             const int r = i / kLT, q = i - r * kLT;
-            float a = 0.f, b = 0.f, aa = 0.f, bb = 0.f, ab = 0.f;
+            float2 m01 = make_float2(0.f, 0.f), m23 = make_float2(0.f, 0.f);
+            float m4 = 0.f;
 #pragma unroll
             for (int t = 0; t < kWin; ++t) {
-                const float xv = sx[r][q + t], yv = sy[r][q + t], k = taps.k[t];
-                a += k * xv;
-                b += k * yv;
-                aa += k * (xv * xv);
-                bb += k * (yv * yv);
-                ab += k * (xv * yv);
+                const float2 v = sxy[r][q + t];
+                const float2 k = make_float2(taps.k[t], taps.k[t]);
+                m01 = __ffma2_rn(k, v, m01);
+                m23 = __ffma2_rn(k, __fmul2_rn(v, v), m23);
+                m4 += taps.k[t] * (v.x * v.y);
             }
-            hs[0][r][q] = a;
-            hs[1][r][q] = b;
-            hs[2][r][q] = aa;
-            hs[3][r][q] = bb;
-            hs[4][r][q] = ab;
+            h01[r][q] = m01;
+            h23[r][q] = m23;
+            h4[r][q] = m4;
         }
         __syncthreads();
         for (int i = threadIdx.x; i < kLT * kLT; i += blockDim.x) {
             const int r = i / kLT, q = i - r * kLT;
             const int u = u0 + r, v = v0 + q;
             if (u >= Hv || v >= Wv) continue;
-            float m[5] = {0.f, 0.f, 0.f, 0.f, 0.f};
+            float2 m01 = make_float2(0.f, 0.f), m23 = make_float2(0.f, 0.f);
+            float m4 = 0.f;
 #pragma unroll
             for (int t = 0; t < kWin; ++t) {
-                const float k = taps.k[t];
-#pragma unroll
-                for (int e = 0; e < 5; ++e) m[e] += k * hs[e][r + t][q];
+                const float2 k = make_float2(taps.k[t], taps.k[t]);
+                m01 = __ffma2_rn(k, h01[r + t][q], m01);
+                m23 = __ffma2_rn(k, h23[r + t][q], m23);
+                m4 += taps.k[t] * h4[r + t][q];
             }
-            const float mux = m[0], muy = m[1];
-            const float sxx = m[2] - mux * mux, syy = m[3] - muy * muy, sxy = m[4] - mux * muy;
+            const float mux = m01.x, muy = m01.y;
+            const float sxx = m23.x - mux * mux, syy = m23.y - muy * muy, sxy_ = m4 - mux * muy;
             const float a1 = 2.f * mux * muy + c1, b1 = mux * mux + muy * muy + c1;
-            const float a2 = 2.f * sxy + c2, b2 = sxx + syy + c2;
+            const float a2 = 2.f * sxy_ + c2, b2 = sxx + syy + c2;
             const float inv = 1.f / (b1 * b2);
             const float smap = (a1 * a2) * inv;
             local += smap;
@@ -109,8 +112,10 @@ __global__ void __launch_bounds__(256) ssim_bwd_kernel(const float *__restrict__
                                                        int H, int W, int xs, Taps taps, float l1_coeff,
                                                        const float *__restrict__ maps, float *__restrict__ dx,
                                                        double *sums) {
-    __shared__ float sm[3][kIn][kIn + 1];
-    __shared__ float hs[3][kIn][kLT + 1];
+    __shared__ float2 sm01[kIn][kIn + 1];  // maps 0 and 1 interleaved (packed FFMA2 blurs)
+    __shared__ float sm2[kIn][kIn + 1];
+    __shared__ float2 hs01[kIn][kLT + 1];
+    __shared__ float hs2[kIn][kLT + 1];
     __shared__ float red[8];
     const int Hv = H - 2 * kHalf, Wv = W - 2 * kHalf;
     const int i0 = blockIdx.y * kLT, j0 = blockIdx.x * kLT;  // full-image tile origin
@@ -123,35 +128,37 @@ __global__ void __launch_bounds__(256) ssim_bwd_kernel(const float *__restrict__
             const int u = i0 - 2 * kHalf + r, v = j0 - 2 * kHalf + q;  // valid-map coordinates
             const bool ok = u >= 0 && v >= 0 && u < Hv && v < Wv;
             const int64_t o = (int64_t)c * plane + (int64_t)u * Wv + v;
-            sm[0][r][q] = ok ? maps[o] : 0.f;
-            sm[1][r][q] = ok ? maps[3 * plane + o] : 0.f;
-            sm[2][r][q] = ok ? maps[6 * plane + o] : 0.f;
+            sm01[r][q] = ok ? make_float2(maps[o], maps[3 * plane + o]) : make_float2(0.f, 0.f);
+            sm2[r][q] = ok ? maps[6 * plane + o] : 0.f;
         }
         __syncthreads();
         for (int i = threadIdx.x; i < kIn * kLT; i += blockDim.x) {
             const int r = i / kLT, q = i - r * kLT;
-            float acc[3] = {0.f, 0.f, 0.f};
+            float2 a01 = make_float2(0.f, 0.f);
+            float a2 = 0.f;
 #pragma unroll
             for (int t = 0; t < kWin; ++t) {
                 const float k = taps.k[kWin - 1 - t];
-#pragma unroll
-                for (int e = 0; e < 3; ++e) acc[e] += k * sm[e][r][q + t];
+                a01 = __ffma2_rn(make_float2(k, k), sm01[r][q + t], a01);
+                a2 += k * sm2[r][q + t];
             }
-#pragma unroll
-            for (int e = 0; e < 3; ++e) hs[e][r][q] = acc[e];
+            hs01[r][q] = a01;
+            hs2[r][q] = a2;
         }
         __syncthreads();
         for (int i = threadIdx.x; i < kLT * kLT; i += blockDim.x) {
             const int r = i / kLT, q = i - r * kLT;
             const int gi = i0 + r, gj = j0 + q;
             if (gi >= H || gj >= W) continue;
-            float acc[3] = {0.f, 0.f, 0.f};
+            float2 a01 = make_float2(0.f, 0.f);
+            float a2 = 0.f;
 #pragma unroll
             for (int t = 0; t < kWin; ++t) {
                 const float k = taps.k[kWin - 1 - t];
-#pragma unroll
-                for (int e = 0; e < 3; ++e) acc[e] += k * hs[e][r + t][q];
+                a01 = __ffma2_rn(make_float2(k, k), hs01[r + t][q], a01);
+                a2 += k * hs2[r + t][q];
             }
+            const float acc[3] = {a01.x, a01.y, a2};
             const int64_t pix = (int64_t)gi * W + gj;
             const int64_t p = pix * xs + c;
             const float xv = x[p], yv = y[pix * 3 + c];
