@@ -60,6 +60,8 @@ def parse():
     ap.add_argument("--render-frames", type=int, default=5)
     ap.add_argument("--cpu-budget-s", type=float, default=60.0)
     ap.add_argument("--no-sweep", action="store_true", help="skip the config-3 TF-sweep render measurement")
+    ap.add_argument("--no-c4", action="store_true", help="skip the config-4 densify/prune training measurement")
+    ap.add_argument("--c4-steps", type=int, default=3)
     ap.add_argument("--sweep-frames", type=int, default=2)
     ap.add_argument("--lanes", type=int, default=3, help="CUDA-stream lanes of the view pipeline")
     ap.add_argument("--backend", choices=("nccl", "gloo"), default="nccl",
@@ -287,8 +289,12 @@ def run_b200(args) -> None:
     e2e = {"value": 1000.0 / e2e_ms, "unit": UNIT, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": 8,
            "ms_per_step": e2e_ms}
 
-    # the config-3 sweep has its own barrier / max-over-ranks: every rank takes part
+    # the config-3 sweep and the config-4 run have their own barriers / max-over-ranks:
+    # every rank takes part
     sweep = None if args.no_sweep else run_sweep(args, dev, rank, world)
+    del trainer, views, targets
+    torch.cuda.empty_cache()
+    c4 = None if args.no_c4 else run_c4(args, dev, rank, world)
 
     if rank != 0:
         dist.destroy_process_group() if world > 1 else None
@@ -335,13 +341,14 @@ def run_b200(args) -> None:
 
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
-        cpu = cpu_baseline_sample(learned, tf, cams[mine[0]], targets[0].cpu().numpy(), args.cpu_budget_s)
+        cpu = cpu_baseline_sample(learned, tf, cams[mine[0]], host_targets[0].numpy(), args.cpu_budget_s)
 
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": max(args.warmup, 3), "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f32+f64", "data": "synthetic (seeded, scenes.py)",
             "config": config_block(world, args.backend), "e2e": e2e, "render_mpx_s": render_mpx_s, "loss": loss_val,
             "gpu_launches": int(launches), "roofline": roof, "kernels": kernels, "render_sweep_c3": sweep,
+            "train_densify_c4": c4,
             "cpu_baseline": cpu,
             "clocks": clk}
     print(json.dumps(line), flush=True)
@@ -391,6 +398,67 @@ def run_sweep(args, dev, rank, world) -> dict:
                         "forward render per (frame, TF), frames sharded across ranks",
             "renders": renders, "ms_per_render": ms / (renders / world), "mpx_s": renders * 1920 * 1080 / (ms / 1e3) / 1e6,
             "tf_frames_per_s": renders / (ms / 1e3), "avg_instances": inst / max(len(mine) * 8, 1)}
+
+
+def run_c4(args, dev, rank, world) -> dict:
+    """Config 4: 200k learned Gaussians fit to renders of a 2M-Gaussian 64-blob set, 64 views
+    per step at 800x800 sharded across ranks, each step with the next of 16 TFs over disjoint
+    scalar ranges, densify/prune every 100 steps (clone/split/prune with optimizer-row edits,
+    on the device).  A bounded sample: `c4_steps` timed steps, then one densify/prune; the
+    amortised rate charges 1/100 of the densify per step."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2504_13339_b200 import scenes
+    from paper_2504_13339_b200.device import DeviceTF, Rasterizer
+    from paper_2504_13339_b200.parallel import shard_views
+    from paper_2504_13339_b200.train import TrainConfig, Trainer, View
+
+    learned, truth, _, cams = scenes.config_scene("c4")
+    n_tf, steps = 16, max(args.c4_steps, 1)
+    tfs = [DeviceTF(scenes.range_tf(500 + k, k / n_tf, (k + 1) / n_tf), dev) for k in range(n_tf)]
+    mine = shard_views(len(cams), rank, world)
+    used = [(s % n_tf) for s in range(steps + 1)]
+    rz = Rasterizer(pooled=True)
+    gt = torch.from_numpy(truth.pack()).to(dev)
+    targets = {}
+    for k in sorted(set(used)):
+        for i in mine:
+            fr = rz.forward(gt, len(truth), tfs[k], cams[i])
+            targets[(k, i)] = fr.out_img.view(cams[i].height, cams[i].width, 3).clone()
+    del rz, gt
+    group = dist.group.WORLD if world > 1 else None
+    tr = Trainer(learned, TrainConfig(iterations=30000), group=group)
+    tr.track_densify(True)
+
+    def views_for(s):
+        k = used[s]
+        return [View(cams[i], tfs[k], targets[(k, i)]) for i in mine]
+
+    tr.step(views_for(0), total_views=len(cams))  # warm-up
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+    e0.record()
+    for s in range(steps):
+        tr.step(views_for(s + 1), total_views=len(cams))
+    e1.record()
+    n_before = tr.n
+    n_after = tr.densify_and_prune(scene_extent=1.0, rng=np.random.default_rng(7), position_lr=1.6e-4)
+    e2.record()
+    torch.cuda.synchronize()
+    step_ms, dens_ms = e0.elapsed_time(e1) / steps, e1.elapsed_time(e2)
+    if world > 1:
+        t = torch.tensor([step_ms, dens_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        step_ms, dens_ms = (float(x) for x in t.tolist())
+    return {"workload": "c4: 200k learned Gaussians, targets from a 2M-Gaussian 64-blob set, 64 views/step at "
+                        "800x800 sharded across ranks, 16 TFs over disjoint scalar ranges cycled per step, "
+                        "densify/prune every 100 steps (amortised)",
+            "steps_per_s": 1000.0 / step_ms, "ms_per_step": step_ms, "densify_ms": dens_ms,
+            "steps_per_s_amortised": 1000.0 / (step_ms + dens_ms / 100.0), "n_before": n_before,
+            "n_after": n_after, "timed_steps": steps}
 
 
 # -- the CPU arm (oracle restatement of the reference algorithm) -------------------------

@@ -102,6 +102,24 @@ def random_tf(seed: int, n_bumps: int | None = None, n_knots: int = N_KNOTS) -> 
     return from_tables(ts, op, ts, rgb)
 
 
+def range_tf(seed: int, lo: float, hi: float, n_bumps: int = 2, n_knots: int = N_KNOTS) -> TransferFunction:
+    """A random TF whose opacity bumps sit inside the scalar range [lo, hi] (config 4 cycles
+    16 of these over disjoint ranges); colour ramp as in random_tf."""
+    rng = np.random.default_rng(seed)
+    ts = np.linspace(0.0, 1.0, n_knots)
+    w = hi - lo
+    centres = rng.uniform(lo + 0.25 * w, hi - 0.25 * w, size=n_bumps)
+    widths = rng.uniform(0.05, 0.15, size=n_bumps) * w
+    heights = rng.uniform(0.5, 1.0, size=n_bumps)
+    op = (heights[None, :] * np.exp(-0.5 * ((ts[:, None] - centres[None, :]) / widths[None, :]) ** 2)).sum(1)
+    op = np.where((ts >= lo) & (ts <= hi), np.clip(op, 0.0, 1.0), 0.0)
+    n_anchor = int(rng.integers(2, 7))
+    at = np.concatenate([[0.0], np.sort(rng.uniform(0.0, 1.0, size=n_anchor - 2)), [1.0]])
+    ac = rng.uniform(0.0, 1.0, size=(n_anchor, 3))
+    rgb = np.stack([np.interp(ts, at, ac[:, c]) for c in range(3)], axis=1)
+    return from_tables(ts, op, ts, rgb)
+
+
 def orbit_cameras(n: int, seed: int, width: int, height: int, radius: float = 3.0,
                   fov_deg: float = 50.0) -> list[Camera]:
     rng = np.random.default_rng(seed)

@@ -228,3 +228,22 @@ def test_two_pixel_backward_matches_four_pixel_backward(monkeypatch):
     for k in O.GRAD_CLASSES:
         a, b = getattr(out[0], k), getattr(out[1], k)
         assert np.abs(a - b).max() <= 1e-5 * max(np.abs(a).max(), 1e-300), k
+
+
+def test_large_image_takes_radix_binning_and_matches_oracle():
+    """2560 x 1600 = 16000 tiles exceeds the counting placement's SMEM cursors, so binning
+    takes the radix path by default; the result is still np.lexsort((depth, tile))'s."""
+    from oracle import vegs_oracle as O
+    from paper_2504_13339_b200.constants import DEFAULT_SETTINGS as S
+
+    gs = scenes.random_gaussians(4000, seed=41)
+    gs.log_scale[:] += 1.5
+    tf = scenes.random_tf(41, 4)
+    cam = scenes.orbit_cameras(1, 42, 2560, 1600)[0]
+    img, st = R.render_with_state(gs, tf, cam, (1.0, 1.0, 1.0), S, False, np.float32)
+    img_o, st_o = O.render_with_state(gs, tf, cam, (1.0, 1.0, 1.0), S, False, np.float32)
+    assert len(st_o["order"]) > 10000
+    assert np.array_equal(st.blend.order, st_o["order"])
+    assert np.array_equal(st.blend.out_last, st_o["out_last"])
+    assert np.array_equal(st.blend.n_contrib, st_o["n_contrib"])
+    assert np.abs(img.rgb - img_o["rgb"]).max() < 1e-5
