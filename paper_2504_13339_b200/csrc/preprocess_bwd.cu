@@ -217,9 +217,12 @@ __global__ void __launch_bounds__(256, VEGS_PBWD_MINB) preprocess_bwd_kernel(
         gpos[k] += -(gl[k] - pl * s.light[k]) / s.dist;
     }
     const double vc = clip01(s.v);
-    const double dO = tf_slope(tab.ts_op, tab.op, tab.k_op, vc);
+    const int jo = slope_segment(tab.ts_op, tab.k_op, vc, tab.inv_op);
+    const double dO = (tab.op[jo + 1] - tab.op[jo]) / (tab.ts_op[jo + 1] - tab.ts_op[jo]);
     double gcv = 0.0;
-    for (int c = 0; c < 3; ++c) gcv += d_ch[c] * tf_slope(tab.ts_col, tab.rgb[c], tab.k_col, vc);
+    const int jc = slope_segment(tab.ts_col, tab.k_col, vc, tab.inv_col);
+    for (int c = 0; c < 3; ++c)
+        gcv += d_ch[c] * ((tab.rgb[c][jc + 1] - tab.rgb[c][jc]) / (tab.ts_col[jc + 1] - tab.ts_col[jc]));
     const double g_v = gcv * (s.ka + s.kd * sa) + d_ab * dO * s.w;
     const double raw_value = g_v * s.v * (1.0 - s.v);
     const double raw_weight = d_ab * s.op * s.w * (1.0 - s.w);

@@ -26,16 +26,36 @@ __device__ __forceinline__ int knot_segment(const double *ts, int k, double x) {
     return lo;
 }
 
+// The same segment from a guess: for (near-)uniform knots j = floor((x - ts[0]) / dt) is
+// exact or one off, and one step each way settles it; anything else falls back to the
+// binary search, so the result is the binary search's for any sorted knots.  x >= ts[0].
+__device__ __forceinline__ int knot_segment_g(const double *ts, int k, double x, double inv_dt) {
+    int j = (int)((x - ts[0]) * inv_dt);
+    j = j < 0 ? 0 : (j > k - 1 ? k - 1 : j);
+    if (ts[j] > x) {
+        --j;
+        if (ts[j] > x) return knot_segment(ts, k, x);
+    } else if (j + 1 < k && ts[j + 1] <= x) {
+        ++j;
+        if (j + 1 < k && ts[j + 1] <= x) return knot_segment(ts, k, x);
+    }
+    return j;
+}
+
 __device__ __forceinline__ double clip01(double v) { return v < 0.0 ? 0.0 : (v > 1.0 ? 1.0 : v); }
+
+// np.interp at x on the segment j found for x (x inside [ts[0], ts[k-1]])
+__device__ __forceinline__ double interp_on(const double *ts, const double *vals, int k, int j, double x) {
+    if (j == k - 1 || ts[j] == x) return vals[j];
+    const double slope = (vals[j + 1] - vals[j]) / (ts[j + 1] - ts[j]);
+    return slope * (x - ts[j]) + vals[j];
+}
 
 __device__ double tf_interp(const double *ts, const double *vals, int k, double x) {
     if (x != x) return x;
     if (x < ts[0]) return vals[0];
     if (x > ts[k - 1]) return vals[k - 1];
-    const int j = knot_segment(ts, k, x);
-    if (j == k - 1 || ts[j] == x) return vals[j];
-    const double slope = (vals[j + 1] - vals[j]) / (ts[j + 1] - ts[j]);
-    return slope * (x - ts[j]) + vals[j];
+    return interp_on(ts, vals, k, knot_segment(ts, k, x), x);
 }
 
 __device__ double tf_slope(const double *ts, const double *vals, int k, double x) {
@@ -44,12 +64,19 @@ __device__ double tf_slope(const double *ts, const double *vals, int k, double x
     return (vals[j + 1] - vals[j]) / (ts[j + 1] - ts[j]);
 }
 
+// segment index of the half-open slope convention (tf_slope) for the table's knots
+__device__ __forceinline__ int slope_segment(const double *ts, int k, double x, double inv_dt) {
+    int j = (x < ts[0]) ? -1 : knot_segment_g(ts, k, x, inv_dt);
+    return j < 0 ? 0 : (j > k - 2 ? k - 2 : j);
+}
+
 __device__ __forceinline__ double sigmoid(double x) { return 1.0 / (1.0 + exp(-x)); }
 
 // TF tables staged in shared memory: [ts_op | op | ts_col | r | g | b]
 struct TFTable {
     const double *ts_op, *op, *ts_col, *rgb[3];
     int k_op, k_col;
+    double inv_op, inv_col;  // (k - 1) / (ts[k-1] - ts[0]): the uniform-spacing segment guess
 };
 
 __device__ TFTable stage_tf(const VegsTF &tf, double *smem) {
@@ -65,6 +92,9 @@ __device__ TFTable stage_tf(const VegsTF &tf, double *smem) {
     t.rgb[0] = t.ts_col + t.k_col;
     t.rgb[1] = t.rgb[0] + t.k_col;
     t.rgb[2] = t.rgb[1] + t.k_col;
+    const double sop = t.ts_op[t.k_op - 1] - t.ts_op[0], scol = t.ts_col[t.k_col - 1] - t.ts_col[0];
+    t.inv_op = sop > 0.0 ? (t.k_op - 1) / sop : 0.0;
+    t.inv_col = scol > 0.0 ? (t.k_col - 1) / scol : 0.0;
     return t;
 }
 
@@ -89,8 +119,23 @@ __device__ void shade_one(const ParamView &P, int64_t g, const TFTable &tf, cons
     s.v = sigmoid(P.raw_value[g]);
     s.w = sigmoid(P.raw_weight[g]);
     const double vc = clip01(s.v);
-    s.op = tf_interp(tf.ts_op, tf.op, tf.k_op, vc);
-    for (int c = 0; c < 3; ++c) s.cmap[c] = tf_interp(tf.ts_col, tf.rgb[c], tf.k_col, vc);
+    // np.interp on both maps (the three colour channels share one segment search)
+    if (vc != vc) {
+        s.op = vc;
+        for (int c = 0; c < 3; ++c) s.cmap[c] = vc;
+    } else {
+        if (vc < tf.ts_op[0]) s.op = tf.op[0];
+        else if (vc > tf.ts_op[tf.k_op - 1]) s.op = tf.op[tf.k_op - 1];
+        else s.op = interp_on(tf.ts_op, tf.op, tf.k_op, knot_segment_g(tf.ts_op, tf.k_op, vc, tf.inv_op), vc);
+        if (vc < tf.ts_col[0]) {
+            for (int c = 0; c < 3; ++c) s.cmap[c] = tf.rgb[c][0];
+        } else if (vc > tf.ts_col[tf.k_col - 1]) {
+            for (int c = 0; c < 3; ++c) s.cmap[c] = tf.rgb[c][tf.k_col - 1];
+        } else {
+            const int j = knot_segment_g(tf.ts_col, tf.k_col, vc, tf.inv_col);
+            for (int c = 0; c < 3; ++c) s.cmap[c] = interp_on(tf.ts_col, tf.rgb[c], tf.k_col, j, vc);
+        }
+    }
     s.alpha_base = s.op * s.w;
     double d[3], nn2 = 0.0, dd2 = 0.0;
     for (int k = 0; k < 3; ++k) {

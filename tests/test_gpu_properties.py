@@ -247,3 +247,27 @@ def test_large_image_takes_radix_binning_and_matches_oracle():
     assert np.array_equal(st.blend.out_last, st_o["out_last"])
     assert np.array_equal(st.blend.n_contrib, st_o["n_contrib"])
     assert np.abs(img.rgb - img_o["rgb"]).max() < 1e-5
+
+
+def test_irregular_tf_knots_match_oracle():
+    """The shading's TF lookup guesses the segment from uniform spacing and corrects it; with
+    irregular knots (some nearly coincident) it must still be np.interp's segment."""
+    from oracle import vegs_oracle as O
+    from paper_2504_13339_b200.constants import DEFAULT_SETTINGS as S
+    from paper_2504_13339_b200.transfer import from_tables
+
+    rng = np.random.default_rng(51)
+    ts = np.array([0.0, 0.02, 0.1, 0.1 + 1e-12, 0.35, 0.36, 0.5, 0.9, 0.97, 1.0])
+    op = rng.uniform(0.0, 1.0, size=ts.size)
+    ts_c = np.array([0.0, 0.3, 0.3 + 1e-9, 0.31, 1.0])
+    rgb = rng.uniform(0.0, 1.0, size=(ts_c.size, 3))
+    tf = from_tables(ts, op, ts_c, rgb)
+    gs = scenes.random_gaussians(3000, seed=52)
+    gs.log_scale[:] += 1.0
+    cam = scenes.orbit_cameras(1, 53, 96, 80)[0]
+    img, st = R.render_with_state(gs, tf, cam, (1.0, 1.0, 1.0), S, False, np.float32)
+    img_o, st_o = O.render_with_state(gs, tf, cam, (1.0, 1.0, 1.0), S, False, np.float32)
+    assert np.array_equal(st.kept, st_o["kept"])
+    assert np.array_equal(st.blend.order, st_o["order"])
+    assert np.array_equal(st.blend.out_last, st_o["out_last"])
+    assert np.abs(img.rgb - img_o["rgb"]).max() < 1e-5
