@@ -139,7 +139,8 @@ int vegs_bin_sort(const uint32_t *tiles, const uint64_t *depth_key, const int32_
 
 /* ---- composite -------------------------------------------------------------------- */
 /* Tile blend on the splat table.  out_img H x W x C, out_t H x W (storage type),
- * out_last H x W int32 (sorted-instance index, -1 = none), n_contrib H x W int32.
+ * out_last H x W int32 (sorted-instance index, -1 = none), n_contrib H x W int32 (may be
+ * NULL: the per-pixel contributor counts are then not computed).
  * tile_order (may be NULL) only permutes the order tiles are launched in. */
 int vegs_composite_forward(const int32_t *tile_start, const int32_t *tile_end,
                            const uint32_t *sorted_gauss, const void *record, const int32_t *rect,

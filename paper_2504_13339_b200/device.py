@@ -161,7 +161,7 @@ class Frame:
     out_img: torch.Tensor
     out_t: torch.Tensor
     out_last: torch.Tensor
-    n_contrib: torch.Tensor
+    n_contrib: torch.Tensor | None
     api: dict = field(default_factory=dict)
     visited: torch.Tensor | None = None  # per-instance bitmask of the latest backward_rows
 
@@ -192,6 +192,7 @@ class Rasterizer:
         self.timer = None  # optional KernelTimer: CUDA events around each launch group
         self.launches = 0  # kernels launched by this rasteriser (see LAUNCHES)
         self.last_counts = (0, 0)  # (kept splats, tile instances) of the latest forward
+        self.contrib_counts = True  # per-pixel contributor counts (the trainer turns them off)
 
     def _run(self, name: str, *args) -> None:
         if self.timer is not None:
@@ -301,7 +302,7 @@ class Rasterizer:
         out_img = A.get("out_img", hw * self.n_ch, self.real)
         out_t = A.get("out_t", hw, self.real)
         out_last = A.get("out_last", hw, torch.int32)
-        n_contrib = A.get("n_contrib", hw, torch.int32)
+        n_contrib = A.get("n_contrib", hw, torch.int32) if self.contrib_counts else None
         bg = (ctypes.c_double * 3)(*[float(x) for x in background])
         self._run("vegs_composite_forward", _p(tile_start), _p(tile_end), _p(sorted_gauss), _p(record), _p(rect),
              self.n_ch, int(self.store_f64), bg, width, height, float(self.settings.alpha_clamp),
@@ -415,6 +416,8 @@ class RenderPipeline:
         main = torch.cuda.current_stream()
         self.lanes = [(main if i == 0 else torch.cuda.Stream(dev), Rasterizer(settings, n_channels, pooled=True))
                       for i in range(max(1, lanes))]
+        for _, rz in self.lanes:
+            rz.contrib_counts = False  # images only
 
     def render(self, params: torch.Tensor, n: int, items, background=(1.0, 1.0, 1.0), on_frame=None) -> int:
         """items: list of (camera, DeviceTF).  on_frame(i, frame) is called (on the frame's

@@ -171,6 +171,7 @@ class _Lane:
 
         self.stream = stream
         self.rz = Rasterizer(tr.settings, 11 if tr.with_aux else 3, store_f64=False, pooled=True)
+        self.rz.contrib_counts = False  # nobody reads them in training
         self.loss = LossKernel(tr.device)
         self.loss_launches = 0
         self.d_img = None
