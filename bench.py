@@ -147,7 +147,8 @@ class KernelTimer:
         ev.record()  # on the current stream = the launching stream
         key = (name, id(rz))
         if begin:
-            self.open[key] = (ev, (rz or self.rz).last_counts)
+            src = rz or self.rz
+            self.open[key] = (ev, src.last_counts if src is not None else (0, 0))
         else:
             start, counts = self.open.pop(key)
             self.done[name].append((start, ev, counts))
@@ -160,6 +161,26 @@ class KernelTimer:
                 out[name] = dict(launches=len(recs), avg_ms=sum(ms) / len(ms), total_ms=sum(ms),
                                  counts=[c for _, _, c in recs])
         return out
+
+
+STAGES = ("vegs_preprocess_forward", "vegs_bin_count", "vegs_bin_sort", "vegs_composite_forward",
+          "vegs_loss_l1_ssim", "vegs_composite_backward", "vegs_preprocess_backward")
+
+
+def stage_bytes(name: str, n: int, n_kept: int, n_inst: int, pixels: int) -> float | None:
+    """Algorithmic HBM bytes per call (with this build's float64
+    parameters and float32 splat table); None where no byte model bounds the stage."""
+    if name == "vegs_preprocess_forward":  # params in; record 48 + rect 16 + tiles 4 + depth key 8 out
+        return float(152 * n + 76 * n)
+    if name == "vegs_bin_sort":  # splat ids in depth order + rects in, one id per instance out
+        return float(20 * n_kept + 4 * n_inst)
+    if name in ("vegs_composite_forward", "vegs_composite_backward"):
+        return algorithmic_bytes(name, n_kept, n_inst, pixels)
+    if name == "vegs_loss_l1_ssim":  # image + target in, gradient out (fused minimum)
+        return float(36 * pixels)
+    if name == "vegs_preprocess_backward":  # params in, gradients read+written, row sums
+        return float(152 * n + 304 * n + 72 * n_kept)
+    return None
 
 
 def algorithmic_bytes(name: str, n_kept: int, n_inst: int, pixels: int, n_ch: int = 3) -> float:
@@ -246,6 +267,37 @@ def run_b200(args) -> None:
     ksum = timer.summary()
     loss_val = float(loss.item())
     trainer.check_finite()
+
+    # ---- per-stage profile, serialised on one stream (the pipelined step overlaps stages,
+    # which would blur per-stage timings): 4 views through every C-ABI stage of a step
+    from paper_2504_13339_b200.device import LossKernel
+
+    stage_timer = KernelTimer(None, names=STAGES)
+    srz = Rasterizer(pooled=True)
+    srz.contrib_counts = False
+    sloss = LossKernel(dev)
+    sgrads = torch.zeros_like(trainer.params)
+    ssums = torch.zeros(2, dtype=torch.float64, device=dev)
+    d_img = torch.empty(1024, 1024, 3, dtype=torch.float32, device=dev)
+    for rep in range(2):  # the first pass grows the pools
+        srz.timer = stage_timer if rep else None
+        sloss.timer = stage_timer if rep else None
+        for v in views[:4]:
+            fr = srz.forward(trainer.params, trainer.n, v.tf, v.camera)
+            sloss(fr.out_img.view(1024, 1024, 3), v.target, 0.8, 0.2, d_img, ssums)
+            srz.backward(fr, d_img, None, sgrads, accumulate=True)
+    torch.cuda.synchronize()
+    stage_timer.rz = srz
+    peak_hbm, _ = peaks()
+    stages = {}
+    for name, rec in stage_timer.summary().items():
+        byts = [stage_bytes(name, trainer.n, nk, ni, 1024 * 1024) for nk, ni in rec["counts"]]
+        st = {"avg_ms": rec["avg_ms"], "calls": rec["launches"]}
+        if byts and byts[0] is not None:
+            gbs = sum(byts) / len(byts) / (rec["avg_ms"] / 1000.0) / 1e9
+            st.update(algorithmic_gb_s=gbs, hbm_frac=gbs / peak_hbm)
+        stages[name] = st
+    del srz, sloss, sgrads
 
     # ---- forward render throughput over the same views (two-lane render pipeline)
     from paper_2504_13339_b200.device import RenderPipeline
@@ -347,7 +399,8 @@ def run_b200(args) -> None:
             "warmup": max(args.warmup, 3), "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f32+f64", "data": "synthetic (seeded, scenes.py)",
             "config": config_block(world, args.backend), "e2e": e2e, "render_mpx_s": render_mpx_s, "loss": loss_val,
-            "gpu_launches": int(launches), "roofline": roof, "kernels": kernels, "render_sweep_c3": sweep,
+            "gpu_launches": int(launches), "roofline": roof, "kernels": kernels, "stages": stages,
+            "render_sweep_c3": sweep,
             "train_densify_c4": c4,
             "cpu_baseline": cpu,
             "clocks": clk}

@@ -377,6 +377,7 @@ class LossKernel:
     def __init__(self, device=None):
         self.device = device or require_cuda()
         self.pool = Pool(self.device)
+        self.timer = None  # optional KernelTimer, as on Rasterizer
 
     def __call__(self, x: torch.Tensor, y: torch.Tensor, w_l1: float, lam: float, d_x: torch.Tensor,
                  sums: torch.Tensor) -> None:
@@ -385,8 +386,12 @@ class LossKernel:
         nbytes = _lib.size_query("vegs_loss_l1_ssim", _p(x), _p(y), h, w, xs, float(w_l1), float(lam), _p(d_x),
                                  _p(sums), tail=(_stream(),))
         ws = self.pool.get("ws", nbytes, torch.uint8)
+        if self.timer is not None:
+            self.timer.mark("vegs_loss_l1_ssim", True)
         call("vegs_loss_l1_ssim", _p(x), _p(y), h, w, xs, float(w_l1), float(lam), _p(d_x), _p(sums), _p(ws),
              ctypes.byref(ctypes.c_size_t(nbytes)), _stream())
+        if self.timer is not None:
+            self.timer.mark("vegs_loss_l1_ssim", False)
 
     def aux(self, planes: torch.Tensor, out_t: torch.Tensor, ref: torch.Tensor, px_scale: float, w_normal: float,
             w_smooth: float, d_planes: torch.Tensor, sums3: torch.Tensor) -> None:

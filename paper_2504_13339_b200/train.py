@@ -229,6 +229,7 @@ class Trainer:
     def set_timer(self, timer) -> None:
         for lane in self.lanes:
             lane.rz.timer = timer
+            lane.loss.timer = timer
 
     @property
     def launches(self) -> int:
