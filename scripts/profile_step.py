@@ -18,6 +18,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--views", type=int, default=16)
     ap.add_argument("--warmup", type=int, default=2)
+    ap.add_argument("--aux", action="store_true", help="the 11-plane with_aux iteration")
     args = ap.parse_args()
     learned, truth, tf, cams = scenes.config_scene("c2")
     cams = cams[:args.views]
@@ -26,7 +27,7 @@ def main():
     gt = torch.from_numpy(truth.pack()).cuda()
     targets = [rz.forward(gt, len(truth), dtf, c).out_img.view(c.height, c.width, 3).clone() for c in cams]
     del rz, gt
-    tr = Trainer(learned, TrainConfig(iterations=30000))
+    tr = Trainer(learned, TrainConfig(iterations=30000), with_aux=args.aux)
     views = [View(c, dtf, t) for c, t in zip(cams, targets)]
     for _ in range(args.warmup):
         tr.step(views, total_views=16)

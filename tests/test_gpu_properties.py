@@ -230,6 +230,46 @@ def test_two_pixel_backward_matches_four_pixel_backward(monkeypatch):
         assert np.abs(a - b).max() <= 1e-5 * max(np.abs(a).max(), 1e-300), k
 
 
+def test_aux_multi_pixel_kernels_match_one_pixel_kernels_and_oracle(monkeypatch):
+    """The 11-plane (with_aux) float32 path runs the two-pixel forward and four-pixel
+    backward templated on the channel count; VEGS_GENERIC_COMPOSITE=1 routes it to the
+    one-pixel kernels.  Forward planes are bitwise equal; gradients agree to float32
+    rounding (different summation order; the suffix term is carried as one scalar), and
+    both equal the oracle within the parity tolerance."""
+    from oracle import vegs_oracle as O
+    from paper_2504_13339_b200.constants import DEFAULT_SETTINGS as S
+
+    gs = scenes.random_gaussians(20_000, seed=41)
+    tf = scenes.random_tf(41, 4)
+    cam = scenes.orbit_cameras(1, 42, 256, 192)[0]
+    rng = np.random.default_rng(43)
+    dg = dict(rgb=rng.uniform(-1, 1, size=(192, 256, 3)), alpha=rng.uniform(-1, 1, size=(192, 256)),
+              depth=rng.uniform(-1, 1, size=(192, 256)), normal=rng.uniform(-1, 1, size=(192, 256, 3)),
+              attrs=rng.uniform(-1, 1, size=(192, 256, 4)))
+    img_o, st_o = O.render_with_state(gs, tf, cam, (1.0, 1.0, 1.0), S, True, np.float32)
+    g_o = O.rasterize_backward(st_o, **dg)
+    out = []
+    for generic in (False, True):
+        if generic:
+            monkeypatch.setenv("VEGS_GENERIC_COMPOSITE", "1")
+        img, st = R.render_with_state(gs, tf, cam, (1.0, 1.0, 1.0), S, True, np.float32)
+        g = R.rasterize_backward(st, R.ImageGradients(**dg))
+        out.append((img, g))
+        for k in O.GRAD_CLASSES:
+            ref = g_o[k]
+            assert np.abs(getattr(g, k) - ref).max() <= 1e-4 * max(np.abs(ref).max(), 1e-300), (generic, k)
+    (ia, ga), (ib, gb) = out
+    for k in ("rgb", "alpha", "depth", "normal", "attrs"):
+        assert np.array_equal(getattr(ia, k), getattr(ib, k)), k
+    for k in ("rgb", "depth", "normal", "attrs"):
+        ref = img_o[k]
+        assert np.abs(getattr(ia, k) - ref).max() <= 1e-4 * max(np.abs(ref).max(), 1.0), k
+    assert np.array_equal(st.blend.out_last, st_o["out_last"])
+    for k in O.GRAD_CLASSES:
+        a, b = getattr(ga, k), getattr(gb, k)
+        assert np.abs(a - b).max() <= 1e-5 * max(np.abs(a).max(), 1e-300), k
+
+
 def test_large_image_takes_radix_binning_and_matches_oracle():
     """2560 x 1600 = 16000 tiles exceeds the counting placement's SMEM cursors, so binning
     takes the radix path by default; the result is still np.lexsort((depth, tile))'s."""
