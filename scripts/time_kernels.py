@@ -1,5 +1,5 @@
 """Quick timing of every C-ABI call of one config-2 view (CUDA events around each call on a
-single stream, forward + backward over 4 views): python scripts/time_kernels.py [reps]"""
+single stream, forward + backward over 4 views): python scripts/time_kernels.py [reps] [channels]"""
 import sys
 from collections import defaultdict
 from pathlib import Path
@@ -14,9 +14,10 @@ from paper_2504_13339_b200.device import DeviceTF, Rasterizer  # noqa: E402
 
 def main():
     reps = int(sys.argv[1]) if len(sys.argv) > 1 else 10
+    n_ch = int(sys.argv[2]) if len(sys.argv) > 2 else 3
     gs, truth, tf, cams = scenes.config_scene("c2")
     dtf = DeviceTF(tf)
-    rz = Rasterizer()
+    rz = Rasterizer(n_channels=n_ch)
     params = torch.from_numpy(gs.pack()).cuda()
     grads = torch.zeros_like(params)
     times = defaultdict(list)
@@ -30,7 +31,7 @@ def main():
             else:
                 times[name].append((self.s, ev))
 
-    d_img = torch.rand(1024, 1024, 3, device="cuda") - 0.5
+    d_img = torch.rand(1024, 1024, n_ch, device="cuda") - 0.5
     for r in range(reps + 2):
         rz.timer = T() if r >= 2 else None
         for cam in cams[:4]:
