@@ -43,7 +43,11 @@ __global__ void __launch_bounds__(256) reduce_rows_kernel(const uint32_t *tiles,
         uint32_t w = __ldg(visited + (p >> 5)) >> sh;
         if (span < 32) w &= (1u << span) - 1u;
         while (w) {  // up to 4 visited rows in flight per round, summed in ascending order
-            constexpr int Q = RS * sizeof(Real) <= 48 ? 4 : 1;  // rgb float32 rows: 4 in flight
+#ifndef VEGS_RR_Q11
+#define VEGS_RR_Q11 4
+#endif
+            // rows in flight: 4 rgb float32 rows, VEGS_RR_Q11 aux float32 rows, 1 float64 row
+            constexpr int Q = RS * sizeof(Real) <= 48 ? 4 : (RS * sizeof(Real) <= 80 ? VEGS_RR_Q11 : 1);
             int b[Q];
 #pragma unroll
             for (int q = 0; q < Q; ++q) {
