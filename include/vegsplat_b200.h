@@ -129,7 +129,8 @@ int vegs_bin_count(const uint32_t *tiles, int64_t n, int64_t *offsets, int64_t *
  * Outputs (n_inst): sorted_gauss (Gaussian id); optional (may be NULL): inst_pid
  * (duplicate-order index) and order (kept index, the reference's `order`);
  * tile_start/tile_end (n_tiles); optional tile_order (n_tiles): tile ids by decreasing
- * instance count, the launch order the compositing kernels accept (scheduling only). */
+ * instance count, the launch order the compositing kernels accept (scheduling only).
+ * n_inst must be < 2^31 (int32 instance positions); larger views return VEGS_ERR_ARG. */
 int vegs_bin_sort(const uint32_t *tiles, const uint64_t *depth_key, const int32_t *rect,
                   const int64_t *offsets, const int64_t *kept_idx, int64_t n, int64_t n_kept,
                   int64_t n_inst, int32_t width, int32_t height, int32_t tile_size,

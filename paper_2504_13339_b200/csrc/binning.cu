@@ -594,7 +594,8 @@ extern "C" int vegs_bin_sort(const uint32_t *tiles, const uint64_t *depth_key, c
                              int32_t *tile_start, int32_t *tile_end, int32_t *tile_order, void *ws,
                              size_t *ws_bytes, void *stream) {
     if (!ws_bytes || tile_size != kTile || width < 1 || height < 1) return VEGS_ERR_ARG;
-    if (n_inst >= (int64_t(1) << 32) || n >= (int64_t(1) << 32)) return VEGS_ERR_ARG;
+    // instance positions are int32 (tile ranges, out_last): at most 2^31 - 1 instances per view
+    if (n_inst > (int64_t)INT32_MAX || n >= (int64_t(1) << 32)) return VEGS_ERR_ARG;
     if (ws && (n > 0) && (!tiles || !depth_key || !rect || !offsets || !kept_idx)) return VEGS_ERR_ARG;
     if (ws && (!tile_start || !tile_end || (n_inst > 0 && !sorted_gauss))) return VEGS_ERR_ARG;
     const int tiles_x = (width + kTile - 1) / kTile, tiles_y = (height + kTile - 1) / kTile;

@@ -63,6 +63,10 @@ def test_bad_arguments_are_rejected_not_thrown():
     with pytest.raises(ValueError):
         _lib.call("vegs_composite_forward", None, None, None, None, None, 3, 0, None, 64, 64, 0.99, 1e-4,
                   None, None, None, None, None, None)
+    # more instances than int32 positions can address: refused before any CUDA call
+    with pytest.raises(ValueError):
+        _lib.size_query("vegs_bin_sort", None, None, None, None, None, 1000, 1000, 2**31, 512, 512, 16, None,
+                        None, None, None, None, None, tail=(None,))
 
 
 def test_parameter_pack_roundtrip():
