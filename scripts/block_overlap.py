@@ -20,7 +20,7 @@ def main():
     ts, te = fr.tile_start.long(), fr.tile_end.long()
     last = fr.out_last.view(1024, 1024).long()
     yy, xx = torch.meshgrid(torch.arange(16, device="cuda"), torch.arange(16, device="cuda"), indexing="ij")
-    n8 = n16 = 0
+    n8 = n16 = n256 = 0
     for t in range(4096):
         s0, s1 = int(ts[t]), int(te[t])
         ty, tx = divmod(t, 64)
@@ -43,8 +43,10 @@ def main():
         b16 = b8.any(2)                                       # (inst, by): 16x8 halves
         n8 += int(b8.sum())
         n16 += int(b16.sum())
+        n256 += int(b16.any(1).sum())
     print(f"(instance, 8x8 block) visits {n8}  (instance, 16x8 block) visits {n16}  "
-          f"ratio {n8 / max(n16, 1):.3f} (2.0 = every 16x8 visit would serve both 8x8 blocks)")
+          f"ratio {n8 / max(n16, 1):.3f} (2.0 = every 16x8 visit would serve both 8x8 blocks); "
+          f"(instance, 16x16 tile) visits {n256}, 16x8/16x16 ratio {n16 / max(n256, 1):.3f}")
 
 
 if __name__ == "__main__":
