@@ -1,5 +1,5 @@
 """Quick timing of every C-ABI call of one config-2 view (CUDA events around each call on a
-single stream, forward + backward over 4 views): python scripts/time_kernels.py [reps] [channels]"""
+single stream, forward + backward over 4 views): python scripts/time_kernels.py [reps] [channels] [f64]"""
 import sys
 from collections import defaultdict
 from pathlib import Path
@@ -15,9 +15,10 @@ from paper_2504_13339_b200.device import DeviceTF, Rasterizer  # noqa: E402
 def main():
     reps = int(sys.argv[1]) if len(sys.argv) > 1 else 10
     n_ch = int(sys.argv[2]) if len(sys.argv) > 2 else 3
+    f64 = len(sys.argv) > 3 and sys.argv[3] == "f64"  # the float64 blend (reference default dtype)
     gs, truth, tf, cams = scenes.config_scene("c2")
     dtf = DeviceTF(tf)
-    rz = Rasterizer(n_channels=n_ch)
+    rz = Rasterizer(n_channels=n_ch, store_f64=f64)
     params = torch.from_numpy(gs.pack()).cuda()
     grads = torch.zeros_like(params)
     times = defaultdict(list)
@@ -31,7 +32,7 @@ def main():
             else:
                 times[name].append((self.s, ev))
 
-    d_img = torch.rand(1024, 1024, n_ch, device="cuda") - 0.5
+    d_img = torch.rand(1024, 1024, n_ch, device="cuda", dtype=torch.float64 if f64 else torch.float32) - 0.5
     for r in range(reps + 2):
         rz.timer = T() if r >= 2 else None
         for cam in cams[:4]:
