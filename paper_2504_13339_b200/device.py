@@ -64,15 +64,38 @@ def _p(t: torch.Tensor | None):
     return None if t is None else ctypes.c_void_p(t.data_ptr())
 
 
-def _stream():
-    return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+try:  # the raw cudaStream_t of the current stream without the Stream object round trip
+    from torch._C import _cuda_getCurrentRawStream as _raw_stream  # noqa: E402
+
+    def _stream():
+        return ctypes.c_void_p(_raw_stream(torch._C._cuda_getDevice()))
+except ImportError:  # pragma: no cover - older torch
+    def _stream():
+        return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
 
 
 def rec_stride(n_ch: int) -> int:
     return ((7 + n_ch) + 3) & ~3
 
 
+_CAMERA_CACHE: dict = {}
+
+
 def camera_struct(cam) -> VegsCamera:
+    """The kernels' camera block (read-only to them); cached per (frozen, hashable) Camera,
+    since views repeat every step and the look-at math is numpy work on the host."""
+    try:
+        c = _CAMERA_CACHE.get(cam)
+    except TypeError:  # a camera with unhashable fields (lists): no caching
+        return _camera_struct(cam)
+    if c is None:
+        if len(_CAMERA_CACHE) >= 4096:
+            _CAMERA_CACHE.clear()
+        c = _CAMERA_CACHE[cam] = _camera_struct(cam)
+    return c
+
+
+def _camera_struct(cam) -> VegsCamera:
     c = VegsCamera()
     c.position[:] = [float(x) for x in cam.position]
     rot = np.asarray(cam.world_to_cam_rotation(), dtype=np.float64).ravel()
