@@ -74,6 +74,25 @@ except ImportError:  # pragma: no cover - older torch
         return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
 
 
+class use_stream:
+    """``torch.cuda.stream(s)`` for the hot host path: the same stream switch without the
+    current-device resolution (single device per process)."""
+
+    __slots__ = ("s", "prev")
+
+    def __init__(self, s):
+        self.s = s
+
+    def __enter__(self):
+        self.prev = torch.cuda.current_stream(self.s.device)
+        torch.cuda.set_stream(self.s)
+        return self.s
+
+    def __exit__(self, *exc):
+        torch.cuda.set_stream(self.prev)
+        return False
+
+
 def rec_stride(n_ch: int) -> int:
     return ((7 + n_ch) + 3) & ~3
 
@@ -212,6 +231,7 @@ class Rasterizer:
         self.store_f64 = store_f64
         self.real = torch.float64 if store_f64 else torch.float32
         self.pool = Pool(self.device) if pooled else None
+        self._count_slots: list = []  # free (pinned counts, event) pairs, see _bin_begin
         self.timer = None  # optional KernelTimer: CUDA events around each launch group
         self.launches = 0  # kernels launched by this rasteriser (see LAUNCHES)
         self.last_counts = (0, 0)  # (kept splats, tile instances) of the latest forward
@@ -285,11 +305,14 @@ class Rasterizer:
         ws = A.get("ws_count", wsz, torch.uint8)
         self._run("vegs_bin_count", _p(tiles), n, _p(offsets), _p(kept_idx), _p(counts), _p(ws),
              ctypes.byref(ctypes.c_size_t(wsz)), s)
-        host = torch.empty(2, dtype=torch.int64, pin_memory=True)
+        # pinned count buffer + event from a free list (a pinned allocation per view costs
+        # ~60 us of host time); returned in forward_end once the host has read the counts
+        slot = self._count_slots.pop() if self._count_slots else (
+            torch.empty(2, dtype=torch.int64, pin_memory=True), torch.cuda.Event())
+        host, ev = slot
         host.copy_(counts, non_blocking=True)
-        ev = torch.cuda.Event()
-        ev.record()
-        return dict(A=A, n=n, record=record, rect=rect, tiles=tiles, depth_key=depth_key, width=width,
+        ev.record(torch.cuda.current_stream(self.device))
+        return dict(slot=slot, A=A, n=n, record=record, rect=rect, tiles=tiles, depth_key=depth_key, width=width,
                     height=height, background=background, cs=cs, tf=tf, params=params, want_order=want_order,
                     api=api, offsets=offsets, kept_idx=kept_idx, host=host, event=ev)
 
@@ -303,6 +326,7 @@ class Rasterizer:
         s = _stream()
         pend["event"].synchronize()
         n_kept, n_inst = (int(x) for x in pend["host"].tolist())
+        self._count_slots.append(pend.pop("slot"))
         self.last_counts = (n_kept, n_inst)
         tiles_x = (width + TILE - 1) // TILE
         n_tiles = tiles_x * ((height + TILE - 1) // TILE)
@@ -335,8 +359,8 @@ class Rasterizer:
                      settings=self.st, bg=bg, params=params, record=record, rect=rect, tiles=tiles,
                      depth_key=depth_key, offsets=offsets, kept_idx=kept_idx, n_kept=n_kept, n_inst=n_inst,
                      sorted_gauss=sorted_gauss, inst_pid=inst_pid, order=order, tile_start=tile_start,
-                     tile_end=tile_end, tile_order=tile_order, out_img=out_img, out_t=out_t, out_last=out_last, n_contrib=n_contrib,
-                     api=api)
+                     tile_end=tile_end, tile_order=tile_order, out_img=out_img, out_t=out_t, out_last=out_last,
+                     n_contrib=n_contrib, api=api)
 
     # -- backward -------------------------------------------------------------------
     def backward_rows(self, fr: Frame, d_img: torch.Tensor, d_alpha: torch.Tensor | None = None) -> torch.Tensor:
@@ -440,8 +464,8 @@ class RenderPipeline:
     Output frames are only valid until the lane that produced them is reused."""
 
     def __init__(self, settings: RasterSettings = DEFAULT_SETTINGS, n_channels: int = 3, lanes: int = 3):
-        dev = require_cuda()
-        main = torch.cuda.current_stream()
+        dev = self.device = require_cuda()
+        main = torch.cuda.current_stream(dev)
         self.lanes = [(main if i == 0 else torch.cuda.Stream(dev), Rasterizer(settings, n_channels, pooled=True))
                       for i in range(max(1, lanes))]
         for _, rz in self.lanes:
@@ -450,7 +474,7 @@ class RenderPipeline:
     def render(self, params: torch.Tensor, n: int, items, background=(1.0, 1.0, 1.0), on_frame=None) -> int:
         """items: list of (camera, DeviceTF).  on_frame(i, frame) is called (on the frame's
         stream) right after each composite.  Returns the total instance count."""
-        main = torch.cuda.current_stream()
+        main = torch.cuda.current_stream(self.device)
         for s, _ in self.lanes[1:]:
             s.wait_stream(main)
         L = len(self.lanes)
@@ -458,7 +482,7 @@ class RenderPipeline:
 
         def begin(i):
             s, rz = self.lanes[i % L]
-            with torch.cuda.stream(s):
+            with use_stream(s):
                 pend[i] = rz.forward_begin(params, n, items[i][1], items[i][0], background)
 
         total = 0
@@ -468,7 +492,7 @@ class RenderPipeline:
             if i + 1 < len(items):
                 begin(i + 1)
             s, rz = self.lanes[i % L]
-            with torch.cuda.stream(s):
+            with use_stream(s):
                 fr = rz.forward_end(pend[i])
                 pend[i] = None
                 total += fr.n_inst

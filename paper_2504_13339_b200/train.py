@@ -23,7 +23,7 @@ import numpy as np
 import torch
 
 from .constants import DEFAULT_SETTINGS, RasterSettings
-from .device import DeviceTF, Rasterizer, adam_step_device, require_cuda
+from .device import DeviceTF, Rasterizer, adam_step_device, require_cuda, use_stream
 from .loss import l1_ssim_device
 from .model import FLOATS_PER_GAUSSIAN, PARAM_CLASSES, GaussianSet, class_offsets
 from .parallel import allreduce_gradients
@@ -217,7 +217,7 @@ class Trainer:
         # Views are pipelined over `lanes` CUDA streams, each with its own scratch pool,
         # loss workspace and gradient buffer: one view's preprocess, count readback and
         # sort overlap the previous view's compositing.  Lane 0 runs on the caller's stream.
-        self.lanes = [_Lane(self, torch.cuda.current_stream() if i == 0 else torch.cuda.Stream(self.device))
+        self.lanes = [_Lane(self, torch.cuda.current_stream(self.device) if i == 0 else torch.cuda.Stream(self.device))
                       for i in range(max(1, lanes))]
         self.lanes[0].grads = self.grads
         self.rz = self.lanes[0].rz
@@ -288,7 +288,7 @@ class Trainer:
              scene_extent: float = 1.0) -> torch.Tensor:
         """One optimisation step over this rank's views; returns the mean loss over
         this rank's views as a device scalar (no host sync besides the per-view counts)."""
-        main = torch.cuda.current_stream()
+        main = torch.cuda.current_stream(self.device)
         total = total_views if total_views is not None else len(views)
         n_v = len(views)
         sums = torch.zeros(n_v, 5, dtype=torch.float64, device=self.device)
@@ -304,7 +304,7 @@ class Trainer:
 
         def begin(i: int) -> None:
             lane = lanes[i % len(lanes)]
-            with torch.cuda.stream(lane.stream):
+            with use_stream(lane.stream):
                 pend[i] = lane.rz.forward_begin(self.params, self.n, views[i].tf, views[i].camera, self.background)
 
         if n_v:
@@ -314,7 +314,7 @@ class Trainer:
                 begin(i + 1)  # queue the next view's preprocess before waiting on this one's count
             k = i % len(lanes)
             lane = lanes[k]
-            with torch.cuda.stream(lane.stream):
+            with use_stream(lane.stream):
                 fr = lane.rz.forward_end(pend[i])
                 pend[i] = None
                 self._loss_and_backward(lane, fr, views[i], 1.0 / total, not used[k], sums[i], *targets[i])

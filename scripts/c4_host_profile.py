@@ -37,7 +37,7 @@ def main():
         tr.step(views)
     torch.cuda.synchronize()
     pr.disable()
-    pstats.Stats(pr).sort_stats("tottime").print_stats(25)
+    pstats.Stats(pr).sort_stats(sys.argv[1] if len(sys.argv) > 1 else "tottime").print_stats(40)
 
 
 if __name__ == "__main__":
