@@ -63,7 +63,7 @@ def parse():
     ap.add_argument("--no-c4", action="store_true", help="skip the config-4 densify/prune training measurement")
     ap.add_argument("--c4-steps", type=int, default=3)
     ap.add_argument("--sweep-frames", type=int, default=2)
-    ap.add_argument("--lanes", type=int, default=3, help="CUDA-stream lanes of the view pipeline")
+    ap.add_argument("--lanes", type=int, default=4, help="CUDA-stream lanes of the view pipeline")
     ap.add_argument("--backend", choices=("nccl", "gloo"), default="nccl",
                     help="gradient all-reduce backend for N>1 (gloo: host-side plumbing check only)")
     return ap.parse_args()
@@ -299,10 +299,10 @@ def run_b200(args) -> None:
         stages[name] = st
     del srz, sloss, sgrads
 
-    # ---- forward render throughput over the same views (two-lane render pipeline)
+    # ---- forward render throughput over the same views (the render pipeline's stream lanes)
     from paper_2504_13339_b200.device import RenderPipeline
 
-    pipe = RenderPipeline()
+    pipe = RenderPipeline(lanes=args.lanes)
     items = [(v.camera, dtf) for v in views]
     for _ in range(2):
         pipe.render(trainer.params, trainer.n, items)
@@ -426,7 +426,7 @@ def run_sweep(args, dev, rank, world) -> dict:
     tfs = {f: [DeviceTF(scenes.random_tf(1000 + 8 * f + k), dev) for k in range(8)] for f in mine}
     from paper_2504_13339_b200.device import RenderPipeline
 
-    pipe = RenderPipeline()
+    pipe = RenderPipeline(lanes=args.lanes)
     items = [(cams[f], tf) for f in mine for tf in tfs[f]]
     # warm-up over every (frame, TF): the scratch pools grow to the largest instance count
     # here, so no allocation happens inside the timed region

@@ -463,7 +463,7 @@ class RenderPipeline:
     count, so the small per-view kernels overlap the previous view's compositing.
     Output frames are only valid until the lane that produced them is reused."""
 
-    def __init__(self, settings: RasterSettings = DEFAULT_SETTINGS, n_channels: int = 3, lanes: int = 3):
+    def __init__(self, settings: RasterSettings = DEFAULT_SETTINGS, n_channels: int = 3, lanes: int = 4):
         dev = self.device = require_cuda()
         main = torch.cuda.current_stream(dev)
         self.lanes = [(main if i == 0 else torch.cuda.Stream(dev), Rasterizer(settings, n_channels, pooled=True))

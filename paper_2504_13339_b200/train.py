@@ -195,7 +195,7 @@ class Trainer:
 
     def __init__(self, gs: GaussianSet, config: TrainConfig, settings: RasterSettings = DEFAULT_SETTINGS,
                  background=(1.0, 1.0, 1.0), l1_weight: float | None = None, group=None, with_aux: bool = False,
-                 lanes: int = 3):
+                 lanes: int = 4):
         self.device = require_cuda()
         self.n = len(gs)
         self.config = config
