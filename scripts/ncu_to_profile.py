@@ -9,8 +9,7 @@ import sys
 from pathlib import Path
 
 NCU = "/usr/local/cuda/bin/ncu"
-NAMES = {"composite_fwd2_kernel": "vegs_composite_forward", "composite_bwd2_kernel": "vegs_composite_backward",
-         "composite_bwd4_kernel": "vegs_composite_backward"}
+NAMES = {"composite_fwd2_kernel": "vegs_composite_forward", "composite_bwd4_kernel": "vegs_composite_backward"}
 
 
 def main(rep, out="profiles/ncu_composite.json"):

@@ -202,10 +202,11 @@ def test_counting_placement_equals_radix_binning(wh, monkeypatch):
         assert torch.equal(a[k], b[k]), k
 
 
-def test_two_pixel_backward_matches_four_pixel_backward(monkeypatch):
-    """The two-pixel-per-lane backward (kept behind VEGS_BWD2) and the default four-pixel
-    one reduce the same per-instance sums in a different order: equal to float32 rounding,
-    and both equal to the oracle."""
+def test_rgb_multi_pixel_kernels_match_one_pixel_kernels_and_oracle(monkeypatch):
+    """The float32 rgb path's two-pixel forward / four-pixel backward against the one-pixel
+    kernels (VEGS_GENERIC_COMPOSITE=1, the reference's loop order per pixel): forward planes
+    bitwise equal, gradients equal to float32 rounding (different summation order), both
+    equal to the oracle."""
     from oracle import vegs_oracle as O
     from paper_2504_13339_b200.constants import DEFAULT_SETTINGS as S
 
@@ -216,17 +217,19 @@ def test_two_pixel_backward_matches_four_pixel_backward(monkeypatch):
     img_o, st_o = O.render_with_state(gs, tf, cam, (1.0, 1.0, 1.0), S, False, np.float32)
     g_o = O.rasterize_backward(st_o, d_rgb)
     out = []
-    for two in (False, True):
-        if two:
-            monkeypatch.setenv("VEGS_BWD2", "1")
+    for generic in (False, True):
+        if generic:
+            monkeypatch.setenv("VEGS_GENERIC_COMPOSITE", "1")
         img, st = R.render_with_state(gs, tf, cam, (1.0, 1.0, 1.0), S, False, np.float32)
         g = R.rasterize_backward(st, R.ImageGradients(rgb=d_rgb))
-        out.append(g)
+        out.append((img, st.blend.out_t, g))
         for k in O.GRAD_CLASSES:
             ref = g_o[k]
-            assert np.abs(getattr(g, k) - ref).max() <= 1e-4 * max(np.abs(ref).max(), 1e-300), (two, k)
+            assert np.abs(getattr(g, k) - ref).max() <= 1e-4 * max(np.abs(ref).max(), 1e-300), (generic, k)
+    (ia, ta, ga), (ib, tb, gb) = out
+    assert np.array_equal(ia.rgb, ib.rgb) and np.array_equal(ta, tb)
     for k in O.GRAD_CLASSES:
-        a, b = getattr(out[0], k), getattr(out[1], k)
+        a, b = getattr(ga, k), getattr(gb, k)
         assert np.abs(a - b).max() <= 1e-5 * max(np.abs(a).max(), 1e-300), k
 
 
