@@ -8,7 +8,7 @@ CUDA device is present, every compute call raises.
 from __future__ import annotations
 
 import ctypes
-from ctypes import POINTER, c_double, c_int32, c_int64, c_size_t, c_uint8, c_uint64, c_void_p
+from ctypes import POINTER, c_double, c_int32, c_int64, c_size_t, c_void_p
 from pathlib import Path
 
 LIB_PATH = Path(__file__).resolve().parent / "lib" / "libvegsplat_b200.so"

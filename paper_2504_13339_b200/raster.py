@@ -24,7 +24,7 @@ from .camera import Camera
 from .constants import DEFAULT_SETTINGS, RasterSettings
 from .device import DeviceTF, Frame, Rasterizer, rec_stride, require_cuda
 from .images import ImageBuffer
-from .model import BETA_MAX, FLOATS_PER_GAUSSIAN, GaussianSet, PARAM_CLASSES
+from .model import BETA_MAX, GaussianSet, PARAM_CLASSES
 from .transfer import TransferFunction
 
 N_AUX_CHANNELS = 11

@@ -24,8 +24,7 @@ import torch
 
 from .constants import DEFAULT_SETTINGS, RasterSettings
 from .device import DeviceTF, Rasterizer, adam_step_device, require_cuda, use_stream
-from .loss import l1_ssim_device
-from .model import FLOATS_PER_GAUSSIAN, PARAM_CLASSES, GaussianSet, class_offsets
+from .model import PARAM_CLASSES, GaussianSet, class_offsets
 from .parallel import allreduce_gradients
 
 ADAM_BETA1 = 0.9

@@ -8,7 +8,6 @@ Bars (BASELINE.json north star):
     blends; the float64 blend path is held to 1e-9).
 """
 
-import math
 
 import numpy as np
 import pytest
