@@ -23,7 +23,10 @@ namespace vegs {
 // blended are read.  The register-heavy chain runs separately.
 
 template <typename Real, int NV>
-__global__ void __launch_bounds__(256) reduce_rows_kernel(const uint32_t *tiles, const int64_t *offsets,
+#ifndef VEGS_RR_T
+#define VEGS_RR_T 64  // small CTAs: the per-Gaussian walks are uneven (3.5 active lanes per warp)
+#endif
+__global__ void __launch_bounds__(VEGS_RR_T) reduce_rows_kernel(const uint32_t *tiles, const int64_t *offsets,
                                                           const Real *rows, int64_t n, const uint32_t *visited,
                                                           double *sums) {
     const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -46,8 +49,11 @@ __global__ void __launch_bounds__(256) reduce_rows_kernel(const uint32_t *tiles,
 #ifndef VEGS_RR_Q11
 #define VEGS_RR_Q11 4
 #endif
-            // rows in flight: 4 rgb float32 rows, VEGS_RR_Q11 aux float32 rows, 1 float64 row
-            constexpr int Q = RS * sizeof(Real) <= 48 ? 4 : (RS * sizeof(Real) <= 80 ? VEGS_RR_Q11 : 1);
+            // rows in flight: VEGS_RR_Q3 rgb float32 rows, VEGS_RR_Q11 aux float32 rows, 1 float64 row
+#ifndef VEGS_RR_Q3
+#define VEGS_RR_Q3 3
+#endif
+            constexpr int Q = RS * sizeof(Real) <= 48 ? VEGS_RR_Q3 : (RS * sizeof(Real) <= 80 ? VEGS_RR_Q11 : 1);
             int b[Q];
 #pragma unroll
             for (int q = 0; q < Q; ++q) {
@@ -278,14 +284,15 @@ extern "C" int vegs_preprocess_backward(const double *params, int64_t n, const V
         return VEGS_ERR_ARG;
     if (n == 0) return VEGS_OK;
     const int blocks = (int)((n + 255) / 256);
+    const int rr_blocks = (int)((n + VEGS_RR_T - 1) / VEGS_RR_T);
     cudaStream_t s = (cudaStream_t)stream;
     double *sums = (double *)ws;
     if (store_f64) {
-        if (n_channels == 3) reduce_rows_kernel<double, 9><<<blocks, 256, 0, s>>>(tiles, offsets, (const double *)inst_rows, n, inst_visited, sums);
-        else reduce_rows_kernel<double, 17><<<blocks, 256, 0, s>>>(tiles, offsets, (const double *)inst_rows, n, inst_visited, sums);
+        if (n_channels == 3) reduce_rows_kernel<double, 9><<<rr_blocks, VEGS_RR_T, 0, s>>>(tiles, offsets, (const double *)inst_rows, n, inst_visited, sums);
+        else reduce_rows_kernel<double, 17><<<rr_blocks, VEGS_RR_T, 0, s>>>(tiles, offsets, (const double *)inst_rows, n, inst_visited, sums);
     } else {
-        if (n_channels == 3) reduce_rows_kernel<float, 9><<<blocks, 256, 0, s>>>(tiles, offsets, (const float *)inst_rows, n, inst_visited, sums);
-        else reduce_rows_kernel<float, 17><<<blocks, 256, 0, s>>>(tiles, offsets, (const float *)inst_rows, n, inst_visited, sums);
+        if (n_channels == 3) reduce_rows_kernel<float, 9><<<rr_blocks, VEGS_RR_T, 0, s>>>(tiles, offsets, (const float *)inst_rows, n, inst_visited, sums);
+        else reduce_rows_kernel<float, 17><<<rr_blocks, VEGS_RR_T, 0, s>>>(tiles, offsets, (const float *)inst_rows, n, inst_visited, sums);
     }
     VEGS_CHECK_LAUNCH();
     const size_t smem = tf_smem_bytes(*tf);
