@@ -22,10 +22,13 @@
 namespace vegs {
 
 template <typename Real>
-#ifndef VEGS_PFWD_MINB
-#define VEGS_PFWD_MINB 4  // 64 registers: 4x the resident warps of the unbounded build, ~2x faster
+#ifndef VEGS_PFWD_T
+#define VEGS_PFWD_T 256
 #endif
-__global__ void __launch_bounds__(256, VEGS_PFWD_MINB) preprocess_fwd_kernel(
+#ifndef VEGS_PFWD_MINB
+#define VEGS_PFWD_MINB (1024 / VEGS_PFWD_T)  // 64 registers: 4x the resident warps of the unbounded build, ~2x faster
+#endif
+__global__ void __launch_bounds__(VEGS_PFWD_T, VEGS_PFWD_MINB) preprocess_fwd_kernel(
     const double *params, int64_t n, VegsCamera cam, VegsTF tf, VegsSettings st, int n_ch,
     VegsSplatTable out) {
     extern __shared__ double tf_smem[];
@@ -171,16 +174,15 @@ extern "C" int vegs_preprocess_forward(const double *params, int64_t n, const Ve
     if (!out->record || !out->rect || !out->tiles || !out->depth_key) return VEGS_ERR_ARG;
     if (n == 0) return VEGS_OK;
     const size_t smem = tf_smem_bytes(*tf);
-    const int blocks = (int)((n + 255) / 256);
     cudaStream_t s = (cudaStream_t)stream;
     if (store_f64) {
         VEGS_CUDA(cudaFuncSetAttribute(preprocess_fwd_kernel<double>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        preprocess_fwd_kernel<double><<<blocks, 256, smem, s>>>(params, n, *cam, *tf, *st, n_channels, *out);
+        preprocess_fwd_kernel<double><<<(int)((n + VEGS_PFWD_T - 1) / VEGS_PFWD_T), VEGS_PFWD_T, smem, s>>>(params, n, *cam, *tf, *st, n_channels, *out);
     } else {
         VEGS_CUDA(cudaFuncSetAttribute(preprocess_fwd_kernel<float>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        preprocess_fwd_kernel<float><<<blocks, 256, smem, s>>>(params, n, *cam, *tf, *st, n_channels, *out);
+        preprocess_fwd_kernel<float><<<(int)((n + VEGS_PFWD_T - 1) / VEGS_PFWD_T), VEGS_PFWD_T, smem, s>>>(params, n, *cam, *tf, *st, n_channels, *out);
     }
     VEGS_CHECK_LAUNCH();
     return VEGS_OK;

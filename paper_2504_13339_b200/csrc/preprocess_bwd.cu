@@ -9,8 +9,11 @@
 
 #include "preprocess_common.cuh"
 
+#ifndef VEGS_PBWD_T
+#define VEGS_PBWD_T 256
+#endif
 #ifndef VEGS_PBWD_MINB
-#define VEGS_PBWD_MINB 4  // 64 registers: 4 CTAs of 256 threads per SM
+#define VEGS_PBWD_MINB (1024 / VEGS_PBWD_T)  // 64 registers: 1024 resident threads per SM
 #endif
 
 namespace vegs {
@@ -83,7 +86,7 @@ __global__ void __launch_bounds__(VEGS_RR_T) reduce_rows_kernel(const uint32_t *
 
 // Backward, part 2: projection and shading adjoints per Gaussian (float64).
 
-__global__ void __launch_bounds__(256, VEGS_PBWD_MINB) preprocess_bwd_kernel(
+__global__ void __launch_bounds__(VEGS_PBWD_T, VEGS_PBWD_MINB) preprocess_bwd_kernel(
     const double *params, int64_t n, VegsCamera cam, VegsTF tf, VegsSettings st, int n_ch,
     const uint32_t *tiles, const double *sums, double scale, int accumulate,
     double *grads, double *vs_norm, uint8_t *visible_out, double *dstats) {
@@ -283,7 +286,6 @@ extern "C" int vegs_preprocess_backward(const double *params, int64_t n, const V
     if (!cam || !st || !tf_ok(tf) || (n > 0 && (!params || !tiles || !offsets || !grads || !inst_rows || !inst_visited)))
         return VEGS_ERR_ARG;
     if (n == 0) return VEGS_OK;
-    const int blocks = (int)((n + 255) / 256);
     const int rr_blocks = (int)((n + VEGS_RR_T - 1) / VEGS_RR_T);
     cudaStream_t s = (cudaStream_t)stream;
     double *sums = (double *)ws;
@@ -297,7 +299,7 @@ extern "C" int vegs_preprocess_backward(const double *params, int64_t n, const V
     VEGS_CHECK_LAUNCH();
     const size_t smem = tf_smem_bytes(*tf);
     VEGS_CUDA(cudaFuncSetAttribute(preprocess_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    preprocess_bwd_kernel<<<blocks, 256, smem, s>>>(params, n, *cam, *tf, *st, n_channels, tiles, sums, scale,
+    preprocess_bwd_kernel<<<(int)((n + VEGS_PBWD_T - 1) / VEGS_PBWD_T), VEGS_PBWD_T, smem, s>>>(params, n, *cam, *tf, *st, n_channels, tiles, sums, scale,
                                                     accumulate, grads, viewspace_norm, visible, densify_stats);
     VEGS_CHECK_LAUNCH();
     return VEGS_OK;
