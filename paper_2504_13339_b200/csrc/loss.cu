@@ -16,8 +16,14 @@
 
 namespace vegs {
 
-constexpr int kWin = 11, kHalf = 5, kLT = 32;  // window, half window, output tile
-constexpr int kIn = kLT + kWin - 1;             // 42: staged input tile side
+#ifndef VEGS_SSIM_TILE
+#define VEGS_SSIM_TILE 32
+#endif
+#ifndef VEGS_SSIM_T
+#define VEGS_SSIM_T 256
+#endif
+constexpr int kWin = 11, kHalf = 5, kLT = VEGS_SSIM_TILE;  // window, half window, output tile
+constexpr int kIn = kLT + kWin - 1;                         // staged input tile side
 
 struct Taps {
     float k[kWin];
@@ -34,7 +40,7 @@ __device__ __forceinline__ float block_sum_f(float v, float *red) {
     return s;
 }
 
-__global__ void __launch_bounds__(256) ssim_fwd_kernel(const float *__restrict__ x, const float *__restrict__ y,
+__global__ void __launch_bounds__(VEGS_SSIM_T) ssim_fwd_kernel(const float *__restrict__ x, const float *__restrict__ y,
                                                        int H, int W, int xs, Taps taps, float c1, float c2,
                                                        float coeff, float *__restrict__ maps, double *sums) {
     // (x, y) pairs interleaved so the two blurs of x and y (and of x^2, y^2) run as packed
@@ -108,7 +114,7 @@ __global__ void __launch_bounds__(256) ssim_fwd_kernel(const float *__restrict__
     if (threadIdx.x == 0) atomicAdd(sums + 1, (double)tot);
 }
 
-__global__ void __launch_bounds__(256) ssim_bwd_kernel(const float *__restrict__ x, const float *__restrict__ y,
+__global__ void __launch_bounds__(VEGS_SSIM_T) ssim_bwd_kernel(const float *__restrict__ x, const float *__restrict__ y,
                                                        int H, int W, int xs, Taps taps, float l1_coeff,
                                                        const float *__restrict__ maps, float *__restrict__ dx,
                                                        double *sums) {
@@ -203,10 +209,10 @@ extern "C" int vegs_loss_l1_ssim(const float *x, const float *y, int32_t height,
     const float l1c = (float)(w_l1 / ((double)height * width * 3.0));
     cudaStream_t s = (cudaStream_t)stream;
     dim3 g1((unsigned)((Wv + kLT - 1) / kLT), (unsigned)((Hv + kLT - 1) / kLT));
-    ssim_fwd_kernel<<<g1, 256, 0, s>>>(x, y, height, width, x_stride, taps, c1, c2, coeff, (float *)ws, sums);
+    ssim_fwd_kernel<<<g1, VEGS_SSIM_T, 0, s>>>(x, y, height, width, x_stride, taps, c1, c2, coeff, (float *)ws, sums);
     VEGS_CHECK_LAUNCH();
     dim3 g2((unsigned)((width + kLT - 1) / kLT), (unsigned)((height + kLT - 1) / kLT));
-    ssim_bwd_kernel<<<g2, 256, 0, s>>>(x, y, height, width, x_stride, taps, l1c, (const float *)ws, d_x, sums);
+    ssim_bwd_kernel<<<g2, VEGS_SSIM_T, 0, s>>>(x, y, height, width, x_stride, taps, l1c, (const float *)ws, d_x, sums);
     VEGS_CHECK_LAUNCH();
     return VEGS_OK;
 }

@@ -9,7 +9,7 @@ import torch
 sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
 
 from paper_2504_13339_b200 import scenes  # noqa: E402
-from paper_2504_13339_b200.device import DeviceTF, Rasterizer  # noqa: E402
+from paper_2504_13339_b200.device import DeviceTF, LossKernel, Rasterizer  # noqa: E402
 
 
 def main():
@@ -33,10 +33,17 @@ def main():
                 times[name].append((self.s, ev))
 
     d_img = torch.rand(1024, 1024, n_ch, device="cuda", dtype=torch.float64 if f64 else torch.float32) - 0.5
+    loss = LossKernel(params.device) if n_ch == 3 and not f64 else None
+    target = torch.rand(1024, 1024, 3, device="cuda")
+    d_loss = torch.empty(1024, 1024, 3, device="cuda")
+    sums = torch.zeros(2, dtype=torch.float64, device="cuda")
     for r in range(reps + 2):
         rz.timer = T() if r >= 2 else None
         for cam in cams[:4]:
             fr = rz.forward(params, len(gs), dtf, cam)
+            if loss is not None:
+                loss.timer = rz.timer
+                loss(fr.out_img.view(1024, 1024, 3), target, 0.8, 0.2, d_loss, sums)
             rz.backward(fr, d_img, None, grads, accumulate=True)
     torch.cuda.synchronize()
     for k, v in times.items():
