@@ -271,7 +271,10 @@ __global__ void chunk_offsets_kernel(uint32_t *counts, const uint32_t *gbase, co
 // walks the chunk's splats in depth order and appends, for the part of each splat's tile
 // rectangle inside its band, the splat id to each tile (distinct tiles inside a splat: no
 // conflicts); per-tile cursors in SMEM.  The bands multiply the warps in flight.
-constexpr int kBands = 4;
+#ifndef VEGS_PLACE_BANDS
+#define VEGS_PLACE_BANDS 8  // warps per chunk CTA, each a band of tile rows
+#endif
+constexpr int kBands = VEGS_PLACE_BANDS;
 __global__ void __launch_bounds__(32 * kBands) place_kernel(const uint32_t *ids, const int4 *rect, int64_t n_kept,
                                                             int C, int tiles_x, int tiles_y, const uint32_t *first,
                                                             uint32_t *sorted_gauss) {
