@@ -270,11 +270,10 @@ __global__ void chunk_offsets_kernel(uint32_t *counts, const uint32_t *gbase, co
 // One CTA per chunk, one warp per horizontal band of tile rows (kBands bands): each warp
 // walks the chunk's splats in depth order and appends, for the part of each splat's tile
 // rectangle inside its band, the splat id to each tile (distinct tiles inside a splat: no
-// conflicts); per-tile cursors in SMEM.  The bands multiply the warps in flight.
-#ifndef VEGS_PLACE_BANDS
-#define VEGS_PLACE_BANDS 8  // warps per chunk CTA, each a band of tile rows
-#endif
-constexpr int kBands = VEGS_PLACE_BANDS;
+// conflicts); per-tile cursors in SMEM.  The bands multiply the warps in flight: 8 for up
+// to 4096 tiles (1024^2: bin_sort 0.419 -> 0.395 ms against 4), 4 above (1080p: the 8-band
+// CTA's 32 KB of cursors per 256 threads cost 2% of the config-3 sweep).
+template <int kBands>
 __global__ void __launch_bounds__(32 * kBands) place_kernel(const uint32_t *ids, const int4 *rect, int64_t n_kept,
                                                             int C, int tiles_x, int tiles_y, const uint32_t *first,
                                                             uint32_t *sorted_gauss) {
@@ -570,8 +569,12 @@ static int bin_place_impl(const uint64_t *depth_key, const int32_t *rect, const 
                                                                      n_tiles, G, tile_end);
         VEGS_CHECK_LAUNCH();
         // 3. placement, one warp per chunk
-        place_kernel<<<n_chunks, 32 * kBands, sizeof(uint32_t) * n_tiles, s>>>(ids, (const int4 *)rect, n_kept, C,
-                                                                              tiles_x, tiles_y, counts, sorted_gauss);
+        if (n_tiles <= 4096)
+            place_kernel<8><<<n_chunks, 32 * 8, sizeof(uint32_t) * n_tiles, s>>>(ids, (const int4 *)rect, n_kept, C,
+                                                                               tiles_x, tiles_y, counts, sorted_gauss);
+        else
+            place_kernel<4><<<n_chunks, 32 * 4, sizeof(uint32_t) * n_tiles, s>>>(ids, (const int4 *)rect, n_kept, C,
+                                                                               tiles_x, tiles_y, counts, sorted_gauss);
         VEGS_CHECK_LAUNCH();
         if (inst_pid || order) {
             placed_extras_kernel<<<(int)((n_inst + 255) / 256), 256, 0, s>>>(
