@@ -505,7 +505,10 @@ static int bin_place_impl(const uint64_t *depth_key, const int32_t *rect, const 
     constexpr int64_t kChunks = VEGS_PLACE_CHUNKS;  // target chunk count: warps for the placement
     const int C = (int)(n_kept > kChunks * 128 ? (n_kept + kChunks - 1) / kChunks : 128);
     const int n_chunks = n_kept > 0 ? (int)((n_kept + C - 1) / C) : 0;
-    const int G = 64, n_groups = (n_chunks + G - 1) / G;
+#ifndef VEGS_PLACE_GROUP
+#define VEGS_PLACE_GROUP 64
+#endif
+    const int G = VEGS_PLACE_GROUP, n_groups = (n_chunks + G - 1) / G;  // chunks per scan group
     size_t t_depth = 0, t_scan = 0, t_tiles = 0;
     {
         cub::DoubleBuffer<uint32_t> dk(nullptr, nullptr), dv(nullptr, nullptr);
