@@ -32,10 +32,16 @@ def main():
     work = np.where(t >= 0, t - ts + 1, 0).astype(np.float64) + 1.0
     n_inst = (te - ts).astype(np.float64)
     print("tiles", len(work), "work mean", work.mean(), "max", work.max(), "p50", np.median(work), "inst mean", n_inst.mean())
+    out = Path("gpurun_out")
+    if out.is_dir():
+        np.savez(out / "tile_work.npz", work=work, n_inst=n_inst)
+    by_count = work[np.argsort(-n_inst, kind="stable")]  # the order binning launches (instance counts)
     for slots in (148 * 6, 148 * 8):
         lb = work.sum() / slots
         nat, lpt = makespan(work, slots), makespan(np.sort(work)[::-1], slots)
-        print(f"slots {slots}: lower bound {lb:.0f}  launch order {nat:.0f} ({nat / lb:.3f})  heaviest-first {lpt:.0f} ({lpt / lb:.3f})")
+        cnt = makespan(by_count, slots)
+        print(f"slots {slots}: lower bound {lb:.0f}  launch order {nat:.0f} ({nat / lb:.3f})  heaviest-first "
+              f"by work {lpt:.0f} ({lpt / lb:.3f})  by instance count {cnt:.0f} ({cnt / lb:.3f})")
 
 
 
