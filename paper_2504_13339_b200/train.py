@@ -295,6 +295,8 @@ class Trainer:
         for lane in lanes[1:]:
             lane.prepare(self)
             lane.stream.wait_stream(main)  # parameters updated, sums zeroed
+        if lanes[0].stream != main:  # called on another stream than the Trainer was built on
+            lanes[0].stream.wait_stream(main)
         lanes[0].grads = self.grads
         lanes[0].dstats = self.densify_stats
         targets = self._upload_targets(views, main)
@@ -318,6 +320,8 @@ class Trainer:
                 pend[i] = None
                 self._loss_and_backward(lane, fr, views[i], 1.0 / total, not used[k], sums[i], *targets[i])
             used[k] = True
+        if lanes[0].stream != main:
+            main.wait_stream(lanes[0].stream)
         if not used[0]:
             self.grads.zero_()
         for k, lane in enumerate(lanes[1:], start=1):

@@ -318,6 +318,33 @@ def test_trainer_host_targets_match_device_targets():
         assert torch.equal(params, runs[0][1])
 
 
+def test_trainer_step_on_another_stream_matches():
+    """step() called under a different current stream than the Trainer was built on (lane 0
+    then is not the caller's stream) gives bitwise the same parameters and losses."""
+    from paper_2504_13339_b200 import scenes
+    from paper_2504_13339_b200.device import DeviceTF
+    from paper_2504_13339_b200.train import Trainer, TrainConfig, View
+
+    d = G.load("train_step")
+    learned = scenes.random_gaussians(2000, seed=0)
+    dtf = DeviceTF(scenes.random_tf(2, 4))
+    cams = scenes.orbit_cameras(2, 3, 64, 64)
+    targets = [torch.from_numpy(d[f"target{i}"]).cuda() for i in range(2)]
+    runs = []
+    for side in (False, True):
+        tr = Trainer(learned, TrainConfig(iterations=100))
+        views = [View(c, dtf, t) for c, t in zip(cams, targets)]
+        s = torch.cuda.Stream()
+        s.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(s if side else torch.cuda.current_stream()):
+            losses = [tr.step(views, iteration=it) for it in (1, 2)]
+            params = tr.params.clone()
+        torch.cuda.synchronize()
+        runs.append(([float(x.item()) for x in losses], params.cpu()))
+    assert runs[1][0] == runs[0][0]
+    assert torch.equal(runs[1][1], runs[0][1])
+
+
 # -- full-size properties (config 2 geometry, one view) ---------------------------------
 
 def test_c2_view_properties():
