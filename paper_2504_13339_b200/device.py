@@ -475,8 +475,9 @@ class RenderPipeline:
         """items: list of (camera, DeviceTF).  on_frame(i, frame) is called (on the frame's
         stream) right after each composite.  Returns the total instance count."""
         main = torch.cuda.current_stream(self.device)
-        for s, _ in self.lanes[1:]:
-            s.wait_stream(main)
+        for i, (s, _) in enumerate(self.lanes):
+            if i or s != main:  # lane 0 is the construction-time stream
+                s.wait_stream(main)
         L = len(self.lanes)
         pend = [None] * len(items)
 
@@ -498,6 +499,7 @@ class RenderPipeline:
                 total += fr.n_inst
                 if on_frame is not None:
                     on_frame(i, fr)
-        for s, _ in self.lanes[1:]:
-            main.wait_stream(s)
+        for i, (s, _) in enumerate(self.lanes):
+            if i or s != main:
+                main.wait_stream(s)
         return total
