@@ -26,6 +26,12 @@
  *   vegs_tf_eval                transfer.py:91-127 eval_opacity / eval_color / d_*_dv
  *   vegs_densify_count / _apply train.py:237-284 densify_and_prune (+ DensifyStats.add :210-214,
  *                               fused into vegs_preprocess_backward)
+ *
+ * Test switches (environment, read at each launch; results are identical either way):
+ *   VEGS_GENERIC_COMPOSITE=1  float32 compositing on the one-pixel kernels instead of the
+ *                             two-pixel forward / four-pixel backward (cross-checks)
+ *   VEGS_BIN_RADIX=1          binning by duplication + radix sort instead of counting
+ *                             placement (the path views above 12288 tiles always take)
  */
 #ifndef VEGSPLAT_B200_H
 #define VEGSPLAT_B200_H
