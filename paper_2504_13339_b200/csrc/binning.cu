@@ -610,7 +610,9 @@ extern "C" int vegs_bin_sort(const uint32_t *tiles, const uint64_t *depth_key, c
     const int tiles_x = (width + kTile - 1) / kTile, tiles_y = (height + kTile - 1) / kTile;
     const int n_tiles = tiles_x * tiles_y;
     cudaStream_t s = (cudaStream_t)stream;
-    if ((tiles_x + 1) * (tiles_y + 1) <= kMaxPlaceTiles && !getenv("VEGS_BIN_RADIX"))
+    const char *radix_env = getenv("VEGS_BIN_RADIX");  // test switch: set and not "0"
+    const bool force_radix = radix_env && radix_env[0] && radix_env[0] != '0';
+    if ((tiles_x + 1) * (tiles_y + 1) <= kMaxPlaceTiles && !force_radix)
         return bin_place_impl(depth_key, rect, offsets, kept_idx, n, n_kept, n_inst, tiles_x, tiles_y, sorted_gauss,
                               inst_pid, order, tile_start, tile_end, tile_order, ws, ws_bytes, s);
     if (n_tiles <= 65536)

@@ -341,7 +341,8 @@ class Rasterizer:
         wsz = _lib.size_query("vegs_bin_sort", *args, tail=(s,))
         ws = A.get("ws_sort", wsz, torch.uint8)
         self._run("vegs_bin_sort", *args, _p(ws), ctypes.byref(ctypes.c_size_t(wsz)), s)
-        if (tiles_x + 1) * ((height + TILE - 1) // TILE + 1) > 12288 or os.environ.get("VEGS_BIN_RADIX"):
+        if (tiles_x + 1) * ((height + TILE - 1) // TILE + 1) > 12288 or \
+                os.environ.get("VEGS_BIN_RADIX", "0") not in ("", "0"):
             self.launches += 1  # radix path
         elif want_order:
             self.launches += 1  # order / inst_pid for the reference-shaped API
