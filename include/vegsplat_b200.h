@@ -23,6 +23,7 @@
  *   vegs_loss_l1_ssim           loss.py:80-168 ssim / ssim_backward / compute_loss (L1 + SSIM part)
  *   vegs_loss_aux               loss.py:175-240 normal-consistency + bilateral-smoothness regularisers
  *   vegs_adam_step              train.py:176-195 adam_step (+ learning_rates :156-173 on the host)
+ *   vegs_adam_step_sum          the same on the sum of the trainer's per-lane gradient buffers
  *   vegs_tf_eval                transfer.py:91-127 eval_opacity / eval_color / d_*_dv
  *   vegs_densify_count / _apply train.py:237-284 densify_and_prune (+ DensifyStats.add :210-214,
  *                               fused into vegs_preprocess_backward)
@@ -251,6 +252,15 @@ int vegs_loss_aux(const float *planes, const float *out_t, const float *ref_rgb,
 int vegs_adam_step(double *params, const double *grads, double *m, double *v, int64_t n,
                    const double *lr, double grad_scale, double bias1, double bias2,
                    int32_t *nonfinite, void *stream);
+
+/* The trainer's step update: g = ((grads0 + grads1) + grads2) + grads3 over the non-NULL
+ * partial buffers (one per stream lane), written back into grads0, then Adam as
+ * vegs_adam_step on g.  params == NULL: only the sum is formed (before a cross-rank
+ * all-reduce; m, v, lr, nonfinite may then be NULL).  Replaces the trainer's eager
+ * per-lane adds in front of train.py:176-195. */
+int vegs_adam_step_sum(double *params, double *grads0, const double *grads1, const double *grads2,
+                       const double *grads3, double *m, double *v, int64_t n, const double *lr,
+                       double grad_scale, double bias1, double bias2, int32_t *nonfinite, void *stream);
 
 /* Library build identity (for the loader's sanity check). */
 const char *vegs_version(void);

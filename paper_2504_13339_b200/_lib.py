@@ -73,6 +73,7 @@ _SIGS = {
     "vegs_loss_l1_ssim": [P, P, c_int32, c_int32, c_int32, c_double, c_double, P, P, P, POINTER(c_size_t), P],
     "vegs_loss_aux": [P, P, P, c_int32, c_int32, c_double, c_double, c_double, P, P, P, POINTER(c_size_t), P],
     "vegs_adam_step": [P, P, P, P, c_int64, P, c_double, c_double, c_double, P, P],
+    "vegs_adam_step_sum": [P, P, P, P, P, P, P, c_int64, P, c_double, c_double, c_double, P, P],
 }
 
 _lib = None

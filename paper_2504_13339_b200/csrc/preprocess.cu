@@ -119,21 +119,35 @@ __global__ void tf_eval_kernel(const double *ts, const double *vals, int k, int 
     }
 }
 
-// Adam over the class-major flat buffer; class boundaries in units of n.
-__constant__ int kClassEnd[10] = {3, 6, 10, 11, 12, 15, 16, 17, 18, 19};
+// Adam over the class-major flat buffer.  blockIdx.y is the unit (0..18) of the 19 n
+// layout, so the class is a table lookup, not a 64-bit division per element.  The step
+// gradient is the sum of up to four per-stream partial buffers, added in a fixed order
+// (((g0 + g1) + g2) + g3) and written back into g0 (the trainer's step gradient).
+__constant__ int kUnitClass[19] = {0, 0, 0, 1, 1, 1, 2, 2, 2, 2, 3, 4, 5, 5, 5, 6, 7, 8, 9};
 
-__global__ void __launch_bounds__(256) adam_kernel(double *params, const double *grads, double *m,
-                                                   double *v, int64_t n, const double *lr,
-                                                   double grad_scale, double bias1, double bias2,
+struct GradParts {
+    double *g0;
+    const double *g[3];
+    int n_extra;
+};
+
+__global__ void __launch_bounds__(256) adam_kernel(double *params, GradParts gp, double *m, double *v, int64_t n,
+                                                   const double *lr, double grad_scale, double bias1, double bias2,
                                                    int *nonfinite) {
-    const int64_t total = 19 * n;
+    const int unit = blockIdx.y;
+    const int cls = kUnitClass[unit];
     const double b1 = 0.9, b2 = 0.999, eps = 1e-15;
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
-         i += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t unit = i / n;
-        int cls = 0;
-        while (unit >= kClassEnd[cls]) ++cls;
-        const double gr = grads[i] * grad_scale;
+    const double lr_c = params ? lr[cls] : 0.0;
+    const int64_t base = (int64_t)unit * n;
+    for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = base + j;
+        double gs = gp.g0[i];
+        if (gp.n_extra > 0) {
+            for (int k = 0; k < gp.n_extra; ++k) gs = gs + gp.g[k][i];
+            gp.g0[i] = gs;
+        }
+        if (!params) continue;  // sum only (before a cross-rank all-reduce)
+        const double gr = gs * grad_scale;
         if (!isfinite(gr)) {
             atomicOr(nonfinite + cls, 1);
             continue;
@@ -145,7 +159,7 @@ __global__ void __launch_bounds__(256) adam_kernel(double *params, const double 
         m[i] = mi;
         v[i] = vi;
         const double upd = (mi / bias1) / (sqrt(vi / bias2) + eps);
-        params[i] = params[i] - lr[cls] * upd;
+        params[i] = params[i] - lr_c * upd;
     }
 }
 
@@ -210,21 +224,40 @@ extern "C" int vegs_splat_table_from_arrays(const double *mean2d, const double *
     return VEGS_OK;
 }
 
+static int adam_launch(double *params, GradParts gp, double *m, double *v, int64_t n, const double *lr,
+                       double grad_scale, double bias1, double bias2, int32_t *nonfinite, void *stream) {
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    int bx = (int)((n + 255) / 256);
+    const int cap = (sms * 8 + 18) / 19;  // ~8 resident 256-thread CTAs per SM over the 19 units
+    if (bx > cap) bx = cap;
+    adam_kernel<<<dim3(bx, 19), 256, 0, (cudaStream_t)stream>>>(params, gp, m, v, n, lr, grad_scale, bias1, bias2,
+                                                                nonfinite);
+    VEGS_CHECK_LAUNCH();
+    return VEGS_OK;
+}
+
 extern "C" int vegs_adam_step(double *params, const double *grads, double *m, double *v, int64_t n,
                               const double *lr, double grad_scale, double bias1, double bias2,
                               int32_t *nonfinite, void *stream) {
     if (n > 0 && (!params || !grads || !m || !v || !lr || !nonfinite)) return VEGS_ERR_ARG;
     if (n == 0) return VEGS_OK;
-    int dev = 0, sms = 148;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    const int64_t total = 19 * n;
-    int blocks = (int)((total + 255) / 256);
-    if (blocks > sms * 16) blocks = sms * 16;
-    adam_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>(params, grads, m, v, n, lr, grad_scale, bias1,
-                                                          bias2, nonfinite);
-    VEGS_CHECK_LAUNCH();
-    return VEGS_OK;
+    GradParts gp{const_cast<double *>(grads), {nullptr, nullptr, nullptr}, 0};  // g0 is only read
+    return adam_launch(params, gp, m, v, n, lr, grad_scale, bias1, bias2, nonfinite, stream);
+}
+
+extern "C" int vegs_adam_step_sum(double *params, double *grads0, const double *grads1, const double *grads2,
+                                  const double *grads3, double *m, double *v, int64_t n, const double *lr,
+                                  double grad_scale, double bias1, double bias2, int32_t *nonfinite, void *stream) {
+    if (n > 0 && !grads0) return VEGS_ERR_ARG;
+    if (n > 0 && params && (!m || !v || !lr || !nonfinite)) return VEGS_ERR_ARG;
+    const double *extra[3] = {grads1, grads2, grads3};
+    GradParts gp{grads0, {nullptr, nullptr, nullptr}, 0};
+    for (int k = 0; k < 3; ++k)
+        if (extra[k]) gp.g[gp.n_extra++] = extra[k];
+    if (n == 0 || (!params && gp.n_extra == 0)) return VEGS_OK;
+    return adam_launch(params, gp, m, v, n, lr, grad_scale, bias1, bias2, nonfinite, stream);
 }
 
 // ---------------------------------------------------------------------------------

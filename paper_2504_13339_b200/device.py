@@ -48,6 +48,7 @@ LAUNCHES = {
     "vegs_loss_l1_ssim": 2,
     "vegs_loss_aux": 3,
     "vegs_adam_step": 1,
+    "vegs_adam_step_sum": 1,
     "vegs_densify_count": 3,
     "vegs_densify_apply": 1,
 }
@@ -342,7 +343,7 @@ class Rasterizer:
         ws = A.get("ws_sort", wsz, torch.uint8)
         self._run("vegs_bin_sort", *args, _p(ws), ctypes.byref(ctypes.c_size_t(wsz)), s)
         if (tiles_x + 1) * ((height + TILE - 1) // TILE + 1) > 12288 or \
-                os.environ.get("VEGS_BIN_RADIX", "0") not in ("", "0"):
+                os.environ.get("VEGS_BIN_RADIX", "")[:1] not in ("", "0"):  # the C rule: set, not '0...'
             self.launches += 1  # radix path
         elif want_order:
             self.launches += 1  # order / inst_pid for the reference-shaped API
@@ -452,10 +453,19 @@ class LossKernel:
 
 
 def adam_step_device(params, grads, m, v, n: int, lrs: torch.Tensor, grad_scale: float, step: int,
-                     nonfinite: torch.Tensor) -> None:
+                     nonfinite: torch.Tensor, extra_grads=()) -> None:
+    """Adam on grads (+ up to three more partial buffers, summed into ``grads`` first in
+    a fixed order); ``params=None`` only forms the sum."""
     b1, b2 = 0.9, 0.999
-    call("vegs_adam_step", _p(params), _p(grads), _p(m), _p(v), n, _p(lrs), float(grad_scale),
-         1.0 - b1 ** step, 1.0 - b2 ** step, _p(nonfinite), _stream())
+    if len(extra_grads) > 3:
+        raise ValueError("at most 4 partial gradient buffers")
+    if params is not None and not extra_grads:
+        call("vegs_adam_step", _p(params), _p(grads), _p(m), _p(v), n, _p(lrs), float(grad_scale),
+             1.0 - b1 ** step, 1.0 - b2 ** step, _p(nonfinite), _stream())
+        return
+    ex = list(extra_grads) + [None] * (3 - len(extra_grads))
+    call("vegs_adam_step_sum", _p(params), _p(grads), _p(ex[0]), _p(ex[1]), _p(ex[2]), _p(m), _p(v), n, _p(lrs),
+         float(grad_scale), 1.0 - b1 ** step, 1.0 - b2 ** step, _p(nonfinite), _stream())
 
 
 class RenderPipeline:
@@ -488,10 +498,11 @@ class RenderPipeline:
                 pend[i] = rz.forward_begin(params, n, items[i][1], items[i][0], background)
 
         total = 0
+        ahead = L > 1  # one lane: item i+1 must not overwrite item i's pooled table early
         if items:
             begin(0)
         for i in range(len(items)):
-            if i + 1 < len(items):
+            if ahead and i + 1 < len(items):
                 begin(i + 1)
             s, rz = self.lanes[i % L]
             with use_stream(s):
@@ -500,6 +511,8 @@ class RenderPipeline:
                 total += fr.n_inst
                 if on_frame is not None:
                     on_frame(i, fr)
+            if not ahead and i + 1 < len(items):
+                begin(i + 1)
         for i, (s, _) in enumerate(self.lanes):
             if i or s != main:
                 main.wait_stream(s)

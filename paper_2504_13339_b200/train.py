@@ -270,6 +270,9 @@ class Trainer:
         if lane.d_img is None or lane.d_img.numel() != img.numel():
             lane.d_img = torch.empty_like(img)
         target = view.target if target is None else target
+        if target.dtype != torch.float32 or tuple(target.shape) != (h, w, 3) or not target.is_contiguous():
+            raise ValueError(f"view target must be a contiguous ({h}, {w}, 3) float32 tensor, got "
+                             f"{tuple(target.shape)} {target.dtype}{'' if target.is_contiguous() else ' (strided)'}")
         if ready is not None:
             lane.stream.wait_event(ready)
         lane.loss(img, target, self.w_l1, self.lam, lane.d_img, sums[:2])
@@ -308,10 +311,13 @@ class Trainer:
             with use_stream(lane.stream):
                 pend[i] = lane.rz.forward_begin(self.params, self.n, views[i].tf, views[i].camera, self.background)
 
+        # With one lane, view i+1 would reuse view i's pooled splat table before view i is
+        # sorted and composited: queue it only after view i's backward is enqueued.
+        ahead = len(lanes) > 1
         if n_v:
             begin(0)
         for i in range(n_v):
-            if i + 1 < n_v:
+            if ahead and i + 1 < n_v:
                 begin(i + 1)  # queue the next view's preprocess before waiting on this one's count
             k = i % len(lanes)
             lane = lanes[k]
@@ -320,31 +326,45 @@ class Trainer:
                 pend[i] = None
                 self._loss_and_backward(lane, fr, views[i], 1.0 / total, not used[k], sums[i], *targets[i])
             used[k] = True
+            if not ahead and i + 1 < n_v:
+                begin(i + 1)
         if lanes[0].stream != main:
             main.wait_stream(lanes[0].stream)
         if not used[0]:
             self.grads.zero_()
-        for k, lane in enumerate(lanes[1:], start=1):
+        for lane in lanes[1:]:
             main.wait_stream(lane.stream)
-            if used[k]:
-                self.grads.add_(lane.grads)
+        # the lanes' partial sums are added inside the Adam kernel (fixed lane order), or in
+        # a sum-only pass of the same kernel before a cross-rank all-reduce
+        extra = [lane.grads for k, lane in enumerate(lanes) if k and used[k]]
+        while len(extra) > 3 or (extra and self.group is not None):
+            adam_step_device(None, self.grads, None, None, self.n, None, 1.0, 1, None, extra[:3])
+            extra = extra[3:]
         allreduce_gradients(self.grads, self.group)
         self.step_count += 1
         it = self.step_count if iteration is None else iteration
         lrs = _lr_tensor(learning_rates(self.config, it, scene_extent), self.device)
         adam_step_device(self.params, self.grads, self.m, self.v, self.n, lrs, 1.0, self.step_count,
-                         self.nonfinite)
+                         self.nonfinite, extra)
         if not views:
             return torch.zeros((), dtype=torch.float64, device=self.device)
-        h, w = views[0].target.shape[:2]
-        n_el = h * w * 3
-        n_pos = (h - 10) * (w - 10) * 3
+        # per-view normalisers (views may differ in resolution): element count, valid SSIM
+        # windows, smoothness pairs (loss.py:146-168, :212-240)
+        hw = [(int(v.camera.height), int(v.camera.width)) for v in views]
+        if all(x == hw[0] for x in hw):
+            (h, w), norm = hw[0], None
+        else:
+            norm = torch.tensor([[h * w * 3, (h - 10) * (w - 10) * 3, 4 * (h * (w - 1) + (h - 1) * w)]
+                                 for h, w in hw], dtype=torch.float64).to(self.device, non_blocking=True)
+        n_el = h * w * 3 if norm is None else norm[:, 0]
+        n_pos = (h - 10) * (w - 10) * 3 if norm is None else norm[:, 1]
+        n_pair = 4 * (h * (w - 1) + (h - 1) * w) if norm is None else norm[:, 2]
         per_view = self.w_l1 * sums[:, 0] / n_el + self.lam * (1.0 - sums[:, 1] / n_pos)
         if self.with_aux:
             cnt = sums[:, 3]
             per_view = per_view + torch.where(cnt > 0, self.config.normal_loss_weight * sums[:, 2] / cnt.clamp(min=1),
                                               torch.zeros_like(cnt))
-            per_view = per_view + self.config.smooth_loss_weight * sums[:, 4] / (4 * (h * (w - 1) + (h - 1) * w))
+            per_view = per_view + self.config.smooth_loss_weight * sums[:, 4] / n_pair
         return per_view.mean()
 
     def track_densify(self, on: bool = True) -> None:

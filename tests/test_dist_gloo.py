@@ -9,6 +9,7 @@ import os
 import socket
 
 import numpy as np
+import pytest
 import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp
@@ -56,12 +57,16 @@ def _free_port():
     return p
 
 
-def test_two_rank_sharded_gradients_equal_single_process_mean():
+@pytest.mark.parametrize("world", [2, 3])
+def test_sharded_gradients_equal_single_process_mean(world):
+    """world 2: shards of 2 + 2 views; world 3: uneven shards of 2 + 1 + 1."""
     gs, tf, cams = _scene()
     full = sum(_view_grad(gs, tf, c, i) for i, c in enumerate(cams)) / len(cams)
+    assert [len(shard_views(len(cams), r, world)) for r in range(world)] == ([2, 2] if world == 2 else [2, 1, 1])
     with mp.Manager() as m:
         out = m.dict()
-        mp.spawn(_worker, args=(2, _free_port(), out), nprocs=2, join=True)
-        r0, r1 = out[0], out[1]
-    assert np.array_equal(r0, r1)  # replicas stay identical
-    assert np.abs(r0 - full).max() <= 1e-12 * max(np.abs(full).max(), 1.0)
+        mp.spawn(_worker, args=(world, _free_port(), out), nprocs=world, join=True)
+        res = [out[r] for r in range(world)]
+    for r in res[1:]:
+        assert np.array_equal(r, res[0])  # replicas stay identical
+    assert np.abs(res[0] - full).max() <= 1e-12 * max(np.abs(full).max(), 1.0)

@@ -1,0 +1,303 @@
+"""Parity at the benchmark's own scale, pinned to the REFERENCE (not only the oracle), and
+the multi-stream paths the benchmark times.
+
+* ``scale_c2_f32`` (tests/golden/make_golden_scale.py): one config-2 view (1M Gaussians,
+  1024 x 1024, float32 blend) rendered and back-propagated by vegsplat itself.  Integer
+  outputs and the float32 T plane are compared through SHA-256 digests (bit-exact), the
+  image and gradients through sampled pixels / rows, inf-norms and sums.
+* ``scale_c3_f32``: a config-3-shaped frame (1920 x 1080, 500k blob Gaussians, the sweep's
+  first TF) through the RenderPipeline the sweep measures.
+* ``densify_stats``: the reference's DensifyStats.add over a 2-view step, against the
+  statistics the trainer fuses into its backward (train.py:210-214).
+* Trainer / RenderPipeline stream lanes (1..4) against single-stream results.
+
+Bars as in test_gpu_parity.py: integers bit-exact, images |d| <= 1e-4 max(|ref|, 1e-3),
+gradients ||d||_inf <= 1e-4 ||ref||_inf per class.
+"""
+
+import hashlib
+
+import numpy as np
+import pytest
+
+import goldens as G
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("needs CUDA", allow_module_level=True)
+
+from oracle import vegs_oracle as O  # noqa: E402
+from paper_2504_13339_b200 import raster as R  # noqa: E402
+from paper_2504_13339_b200 import scenes  # noqa: E402
+from paper_2504_13339_b200.constants import DEFAULT_SETTINGS as S  # noqa: E402
+from paper_2504_13339_b200.device import DeviceTF, Rasterizer, RenderPipeline  # noqa: E402
+from paper_2504_13339_b200.model import PARAM_CLASSES  # noqa: E402
+from paper_2504_13339_b200.train import TrainConfig, Trainer, View  # noqa: E402
+
+IMG_REL = 1e-4
+GRAD_REL = 1e-4
+
+
+def digest(a, dtype) -> np.ndarray:
+    b = np.ascontiguousarray(np.asarray(a).astype(np.dtype(dtype).newbyteorder("<"), copy=False)).tobytes()
+    return np.frombuffer(hashlib.sha256(b).digest(), dtype=np.uint8)
+
+
+def img_close(a, b, rel=IMG_REL):
+    a = np.asarray(a, dtype=np.float64)
+    b = np.asarray(b, dtype=np.float64)
+    return bool(np.all(np.abs(a - b) <= rel * np.maximum(np.abs(b), 1e-3)))
+
+
+def _check_forward_scale(d, img, st):
+    b = st.blend
+    pix = d["pix"]
+    assert len(st.kept) == int(d["n_kept"]) and len(b.order) == int(d["n_inst"])
+    # diagnostics first (sampled), then the full-array digests
+    assert np.array_equal(b.out_last.reshape(-1)[pix], d["pix_last"])
+    assert np.array_equal(b.n_contrib.reshape(-1)[pix], d["pix_ncon"])
+    assert np.array_equal(b.out_t.reshape(-1)[pix], d["pix_t"])
+    assert np.array_equal(b.tile_start, d["tile_start"]) and np.array_equal(b.tile_end, d["tile_end"])
+    assert np.array_equal(digest(st.kept, np.int64), d["kept_sha"])
+    assert np.array_equal(digest(st.proj.rect, np.int32), d["rect_sha"])
+    assert np.array_equal(digest(b.order, np.int64), d["order_sha"])
+    assert np.array_equal(digest(b.out_last, np.int64), d["out_last_sha"])
+    assert np.array_equal(digest(b.n_contrib, np.int32), d["n_contrib_sha"])
+    assert np.array_equal(digest(b.out_t, np.float32), d["out_t_sha"])
+    assert img_close(img.rgb.reshape(-1, 3)[pix], d["pix_rgb"])
+    assert img_close(img.alpha.reshape(-1)[pix], d["pix_alpha"], rel=1e-3)
+    assert abs(float(img.rgb.astype(np.float64).sum()) - float(d["rgb_sum"])) <= 1e-5 * abs(float(d["rgb_sum"]))
+
+
+@pytest.fixture(scope="module")
+def c2_ref():
+    d = G.load("scale_c2_f32")
+    gs, _, tf, cams = scenes.config_scene("c2")
+    cam = G.cam_of(d["cam"])
+    assert cam == cams[0]
+    img, st = R.render_with_state(gs, tf, cam, (1.0, 1.0, 1.0), S, False, np.float32)
+    return d, gs, cam, img, st
+
+
+@pytest.mark.slow
+def test_c2_view_bit_exact_vs_reference(c2_ref):
+    """One benchmark view against vegsplat: kept set, rects, instance order, tile ranges,
+    last contributor, contributor count and T bit-exact; image within the bar."""
+    d, gs, cam, img, st = c2_ref
+    assert len(st.blend.order) > 10_000_000
+    _check_forward_scale(d, img, st)
+
+
+@pytest.mark.slow
+def test_c2_view_gradients_vs_reference(c2_ref):
+    d, gs, cam, img, st = c2_ref
+    h, w = cam.height, cam.width
+    prng = np.random.default_rng(6)
+    probe = dict(rgb=prng.uniform(-1, 1, size=(h, w, 3)), alpha=prng.uniform(-1, 1, size=(h, w)))
+    g = R.rasterize_backward(st, R.ImageGradients(**probe))
+    rows = d["grad_rows"]
+    n = len(gs)
+    for k in PARAM_CLASSES:
+        ref_inf = float(d[f"grad_{k}_inf"])
+        mine = getattr(g, k).reshape(n, -1)
+        assert abs(float(np.abs(mine).max()) - ref_inf) <= GRAD_REL * ref_inf, k
+        assert np.abs(mine[rows] - d[f"grad_{k}_rows"]).max() <= GRAD_REL * ref_inf, k
+        # whole-array aggregates: the sum of magnitudes pins every row, not just the sample
+        ref_abs = float(d[f"grad_{k}_abssum"])
+        assert abs(float(np.abs(mine).sum()) - ref_abs) <= GRAD_REL * ref_abs, k
+        assert abs(float(mine.sum()) - float(d[f"grad_{k}_sum"])) <= GRAD_REL * ref_abs, k
+    assert np.array_equal(digest(g.visible, np.uint8), d["visible_sha"])
+    vsn_inf = float(d["vsn_inf"])
+    assert np.abs(g.viewspace_norm[rows] - d["vsn_rows"]).max() <= GRAD_REL * vsn_inf
+
+
+@pytest.mark.slow
+def test_c3_frame_through_render_pipeline_vs_reference():
+    """A config-3-shaped frame (1920 x 1080, 500k blob Gaussians, the sweep's first TF)
+    rendered by the RenderPipeline the sweep times, against vegsplat's frame: T bit-exact
+    (digest), image within the bar; the frame's integer outputs through the API path."""
+    d = G.load("scale_c3_f32")
+    gs = scenes.blob_gaussians(500_000, seed=1)
+    cam = G.cam_of(d["cam"])
+    tf = scenes.random_tf(1000)
+    img, st = R.render_with_state(gs, tf, cam, (1.0, 1.0, 1.0), S, False, np.float32)
+    _check_forward_scale(d, img, st)
+    params = torch.from_numpy(gs.pack()).cuda()
+    dtf = DeviceTF(tf)
+    other = DeviceTF(scenes.random_tf(1001))
+    got = {}
+
+    def keep(i, fr):
+        got[i] = (fr.out_img.view(cam.height, cam.width, 3).clone(), fr.out_t.view(cam.height, cam.width).clone())
+
+    pipe = RenderPipeline(lanes=3)
+    pipe.render(params, len(gs), [(cam, other), (cam, dtf), (cam, other), (cam, dtf)], on_frame=keep)
+    torch.cuda.synchronize()
+    for i in (1, 3):
+        rgb, t = (x.cpu().numpy() for x in got[i])
+        assert np.array_equal(digest(t, np.float32), d["out_t_sha"]), i
+        assert img_close(rgb.reshape(-1, 3)[d["pix"]], d["pix_rgb"]), i
+
+
+@pytest.mark.parametrize("lanes", [1, 2, 3, 4])
+def test_render_pipeline_frames_equal_single_stream(lanes):
+    """RenderPipeline (the render / sweep benchmark path) gives, per (camera, TF) item and
+    for any lane count, bitwise the frame of a single-stream Rasterizer.forward; items of
+    different sizes exercise the pooled-buffer reuse across lanes."""
+    gs = scenes.blob_gaussians(60_000, seed=1)
+    params = torch.from_numpy(gs.pack()).cuda()
+    cams = scenes.orbit_cameras(3, 5, 320, 200) + scenes.orbit_cameras(2, 6, 96, 160)
+    tfs = [DeviceTF(scenes.random_tf(1000 + k)) for k in range(3)]
+    items = [(cams[i % len(cams)], tfs[i % len(tfs)]) for i in range(7)]
+    ref = []
+    rz = Rasterizer(pooled=False)
+    for cam, tf in items:
+        fr = rz.forward(params, len(gs), tf, cam)
+        ref.append((fr.out_img.clone(), fr.out_t.clone(), fr.out_last.clone()))
+    got = {}
+
+    def keep(i, fr):
+        got[i] = (fr.out_img.clone(), fr.out_t.clone(), fr.out_last.clone())
+
+    pipe = RenderPipeline(lanes=lanes)
+    for _ in range(2):  # the second pass reuses every lane's grown pools
+        got.clear()
+        total = pipe.render(params, len(gs), items, on_frame=keep)
+        torch.cuda.synchronize()
+        assert total > 0
+        for i, (img, t, last) in enumerate(ref):
+            gi, gt, gl = got[i]
+            assert torch.equal(gi, img) and torch.equal(gt, t) and torch.equal(gl, last), (lanes, i)
+
+
+def _train_scene(n_views, w=64, h=64):
+    learned = scenes.random_gaussians(2000, seed=0)
+    truth = scenes.random_gaussians(2000, seed=1)
+    dtf = DeviceTF(scenes.random_tf(2, 4))
+    cams = scenes.orbit_cameras(n_views, 3, w, h)
+    rz = Rasterizer(pooled=False)
+    gt = torch.from_numpy(truth.pack()).cuda()
+    targets = [rz.forward(gt, len(truth), dtf, c).out_img.view(c.height, c.width, 3).clone() for c in cams]
+    return learned, dtf, cams, targets
+
+
+def test_trainer_gradient_buffer_matches_reference_before_adam():
+    """The step's gradient buffer (mean of the per-view gradients, before Adam) against the
+    reference's per-view rasterize_backward of its L1+SSIM gradient, at the 1e-4 bar."""
+    d = G.load("train_step")
+    learned = scenes.random_gaussians(2000, seed=0)
+    dtf = DeviceTF(scenes.random_tf(2, 4))
+    cams = scenes.orbit_cameras(2, 3, 64, 64)
+    for lanes in (1, 4):
+        tr = Trainer(learned, TrainConfig(iterations=100), lanes=lanes)
+        views = [View(c, dtf, torch.from_numpy(d[f"target{i}"]).cuda()) for i, c in enumerate(cams)]
+        tr.step(views, iteration=1)
+        g = tr.grads.cpu().numpy()
+        from paper_2504_13339_b200.model import GaussianSet
+
+        gg = GaussianSet.unpack(g, len(learned))
+        for k in PARAM_CLASSES:
+            assert G.norm_rel(getattr(gg, k), d["grad_" + k]) <= GRAD_REL, (lanes, k)
+
+
+def test_trainer_densify_stats_match_reference():
+    """DensifyStats.add (train.py:210-214) over a 2-view step, fused into the device
+    backward, against the reference's statistics on the same views."""
+    d = G.load("densify_stats")
+    learned = scenes.random_gaussians(2000, seed=0)
+    dtf = DeviceTF(scenes.random_tf(2, 4))
+    cams = scenes.orbit_cameras(2, 3, 64, 64)
+    for lanes in (1, 2, 4):
+        tr = Trainer(learned, TrainConfig(iterations=100), lanes=lanes)
+        tr.track_densify()
+        views = [View(c, dtf, torch.from_numpy(d[f"target{i}"]).cuda()) for i, c in enumerate(cams)]
+        tr.step(views, iteration=1)
+        st = tr.gather_densify_stats().view(-1, 5).cpu().numpy()
+        assert np.array_equal(st[:, 4], d["count"]), lanes
+        assert G.norm_rel(st[:, 0], d["grad_accum"]) <= GRAD_REL, lanes
+        assert G.norm_rel(st[:, 1:4], d["pos_accum"]) <= GRAD_REL, lanes
+
+
+def test_trainer_lane_counts_agree():
+    """Trainer.step with 1, 2, 3 or 4 stream lanes: losses bitwise equal (per-view sums),
+    gradient buffers equal up to float64 summation order, and bitwise equal where the
+    per-lane partial sums coincide (2 views on >= 2 lanes vs 1 lane)."""
+    learned, dtf, cams, targets = _train_scene(5)
+    res = {}
+    for lanes in (1, 2, 3, 4):
+        tr = Trainer(learned, TrainConfig(iterations=100), lanes=lanes)
+        views = [View(c, dtf, t) for c, t in zip(cams, targets)]
+        losses = [float(tr.step(views, iteration=it).item()) for it in (1, 2)]
+        res[lanes] = (losses, tr.grads.clone(), tr.params.clone())
+    l1, g1, p1 = res[1]
+    for lanes in (2, 3, 4):
+        ll, gl, pl = res[lanes]
+        assert abs(ll[0] - l1[0]) <= 1e-12 * abs(l1[0])
+        assert float((gl - g1).abs().max()) <= 1e-12 * float(g1.abs().max()), lanes
+        assert float((pl - p1).abs().max()) <= 1e-9, lanes
+    two = {}
+    for lanes in (1, 2, 4):
+        tr = Trainer(learned, TrainConfig(iterations=100), lanes=lanes)
+        views = [View(c, dtf, t) for c, t in zip(cams[:2], targets[:2])]
+        loss = float(tr.step(views, iteration=1).item())
+        two[lanes] = (loss, tr.params.clone())
+    for lanes in (2, 4):
+        assert two[lanes][0] == two[1][0] and torch.equal(two[lanes][1], two[1][1]), lanes
+
+
+def test_trainer_rejects_malformed_targets():
+    learned, dtf, cams, targets = _train_scene(1)
+    tr = Trainer(learned, TrainConfig(iterations=100))
+    for bad in (targets[0].double(), targets[0].permute(1, 0, 2), torch.zeros(64, 64, 4, device="cuda")):
+        with pytest.raises(ValueError):
+            tr.step([View(cams[0], dtf, bad)])
+
+
+def test_trainer_mixed_resolution_loss_uses_per_view_normalisers():
+    """Views of different sizes in one step: the returned loss is the mean of each view's
+    own normalised loss (each view alone gives its own value)."""
+    learned = scenes.random_gaussians(2000, seed=0)
+    truth = scenes.random_gaussians(2000, seed=1)
+    dtf = DeviceTF(scenes.random_tf(2, 4))
+    cams = [scenes.orbit_cameras(1, 3, 64, 64)[0], scenes.orbit_cameras(1, 4, 96, 48)[0]]
+    rz = Rasterizer(pooled=False)
+    gt = torch.from_numpy(truth.pack()).cuda()
+    views = [View(c, dtf, rz.forward(gt, len(truth), dtf, c).out_img.view(c.height, c.width, 3).clone())
+             for c in cams]
+    alone = [float(Trainer(learned, TrainConfig(iterations=100)).step([v], iteration=1).item()) for v in views]
+    both = float(Trainer(learned, TrainConfig(iterations=100)).step(views, iteration=1).item())
+    assert abs(both - 0.5 * (alone[0] + alone[1])) <= 1e-12 * abs(both)
+
+
+def test_adam_lane_sum_equals_eager_adds():
+    """vegs_adam_step_sum (lane partial sums folded into Adam) is bitwise the eager
+    ((g0 + g1) + g2) + g3 followed by vegs_adam_step."""
+    from paper_2504_13339_b200.device import adam_step_device
+
+    n = 5003
+    gen = torch.Generator(device="cuda").manual_seed(3)
+    p = torch.randn(19 * n, dtype=torch.float64, device="cuda", generator=gen)
+    gs = [torch.randn(19 * n, dtype=torch.float64, device="cuda", generator=gen) for _ in range(4)]
+    m = torch.rand(19 * n, dtype=torch.float64, device="cuda", generator=gen)
+    v = torch.rand(19 * n, dtype=torch.float64, device="cuda", generator=gen)
+    lrs = torch.linspace(1e-4, 1e-2, 10, dtype=torch.float64, device="cuda")
+    bad = torch.zeros(10, dtype=torch.int32, device="cuda")
+    for k in (1, 2, 3, 4):
+        a = [x.clone() for x in (p, m, v)]
+        b = [x.clone() for x in (p, m, v)]
+        g_eager = gs[0].clone()
+        for x in gs[1:k]:
+            g_eager.add_(x)
+        adam_step_device(a[0], g_eager, a[1], a[2], n, lrs, 1.0, 3, bad)
+        g_fused = gs[0].clone()
+        adam_step_device(b[0], g_fused, b[1], b[2], n, lrs, 1.0, 3, bad, [x for x in gs[1:k]])
+        assert torch.equal(g_fused, g_eager), k
+        for x, y in zip(a, b):
+            assert torch.equal(x, y), k
+        # sum only
+        g_sum = gs[0].clone()
+        adam_step_device(None, g_sum, None, None, n, None, 1.0, 1, None, [x for x in gs[1:k]])
+        assert torch.equal(g_sum, g_eager), k
+    assert not bad.any()
