@@ -59,7 +59,7 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--render-frames", type=int, default=5)
     ap.add_argument("--cpu-budget-s", type=float, default=60.0)
-    ap.add_argument("--ref-budget-s", type=float, default=240.0,
+    ap.add_argument("--ref-budget-s", type=float, default=300.0,
                     help="--impl reference: stop timing further views of the step after this many seconds")
     ap.add_argument("--no-sweep", action="store_true", help="skip the config-3 TF-sweep render measurement")
     ap.add_argument("--no-c4", action="store_true", help="skip the config-4 densify/prune training measurement")
@@ -133,7 +133,7 @@ class ClockSampler:
 class KernelTimer:
     """Events recorded on the current stream around each C-ABI launch group."""
 
-    def __init__(self, rz, names=("vegs_composite_forward", "vegs_composite_backward")):
+    def __init__(self, rz, names=("vegs_composite_forward", "vegs_composite_forward_fast", "vegs_composite_backward")):
         import torch
 
         self.torch = torch
@@ -166,6 +166,7 @@ class KernelTimer:
 
 
 STAGES = ("vegs_preprocess_forward", "vegs_bin_count", "vegs_bin_sort", "vegs_composite_forward",
+          "vegs_composite_forward_fast",
           "vegs_loss_l1_ssim", "vegs_composite_backward", "vegs_preprocess_backward")
 
 
@@ -176,7 +177,7 @@ def stage_bytes(name: str, n: int, n_kept: int, n_inst: int, pixels: int) -> flo
         return float(152 * n + 76 * n)
     if name == "vegs_bin_sort":  # splat ids in depth order + rects in, one id per instance out
         return float(20 * n_kept + 4 * n_inst)
-    if name in ("vegs_composite_forward", "vegs_composite_backward"):
+    if name in ("vegs_composite_forward", "vegs_composite_forward_fast", "vegs_composite_backward"):
         return algorithmic_bytes(name, n_kept, n_inst, pixels)
     if name == "vegs_loss_l1_ssim":  # image + target in, gradient out (fused minimum)
         return float(36 * pixels)
@@ -288,7 +289,7 @@ def run_b200(args) -> None:
     from paper_2504_13339_b200.device import LossKernel
 
     stage_timer = KernelTimer(None, names=STAGES)
-    srz = Rasterizer(pooled=True)
+    srz = Rasterizer(pooled=True, fast_t=trainer.fast_t)
     srz.contrib_counts = False
     sloss = LossKernel(dev)
     sgrads = torch.zeros_like(trainer.params)

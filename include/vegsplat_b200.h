@@ -16,6 +16,7 @@
  *   vegs_bin_count / vegs_bin_sort
  *                               raster/pipeline.py:163-194 _build_instances (repeat + lexsort + searchsorted)
  *   vegs_composite_forward      raster/pipeline.py:197-237 rasterize_forward (tile blend on the splat table)
+ *   vegs_composite_forward_fast the same with T carried in float32 (exact decisions; training / render path)
  *   vegs_composite_backward     raster/pipeline.py:291-305 (blend_backward on the splat table, per-instance
  *                               rows written in duplicate order for the deterministic reduction)
  *   vegs_preprocess_backward    raster/pipeline.py:307-366 (np.add.at reduction, project_backward
@@ -27,12 +28,15 @@
  *   vegs_tf_eval                transfer.py:91-127 eval_opacity / eval_color / d_*_dv
  *   vegs_densify_count / _apply train.py:237-284 densify_and_prune (+ DensifyStats.add :210-214,
  *                               fused into vegs_preprocess_backward)
+ *   vegs_tf_max_opacity         BASELINE config 4's prune criterion (max TF opacity per Gaussian)
  *
  * Test switches (environment, read at each launch; results are identical either way):
  *   VEGS_GENERIC_COMPOSITE=1  float32 compositing on the one-pixel kernels instead of the
  *                             two-pixel forward / four-pixel backward (cross-checks)
  *   VEGS_BIN_RADIX=1          binning by duplication + radix sort instead of counting
  *                             placement (the path views above 12288 tiles always take)
+ *   VEGS_FAST_T_DEFER_ALL=1   vegs_composite_forward_fast hands every terminating pixel to its
+ *                             float64 fix-up pass (exercises the fix-up)
  */
 #ifndef VEGSPLAT_B200_H
 #define VEGSPLAT_B200_H
@@ -157,6 +161,22 @@ int vegs_composite_forward(const int32_t *tile_start, const int32_t *tile_end,
                            void *out_t, int32_t *out_last, int32_t *n_contrib,
                            const int32_t *tile_order, void *stream);
 
+/* vegs_composite_forward for float32 splat tables with the transmittance chain in float32
+ * (FFMA2 / MUFU) instead of float64.  Every decision of the reference stays exact -- the
+ * 1/255 skip (float32 guard band, float64 inside it), the alpha clamp (float64 for the
+ * instances that can reach it) and the 1e-4 termination (a rigorous per-pixel bound on
+ * the float32 T error; a pixel whose test falls inside it is re-blended from its tile start
+ * in float64 by a fix-up kernel) -- so out_last and n_contrib equal vegs_composite_forward's
+ * and the reference's; out_t and out_img carry the float32 chain's rounding (~1e-6
+ * relative).  defer: 1 + width * height int32 scratch; defer[0] receives the number of
+ * re-blended pixels.  Replaces the same pipeline.py:197-237 / kernels.py:26-100 call. */
+int vegs_composite_forward_fast(const int32_t *tile_start, const int32_t *tile_end,
+                                const uint32_t *sorted_gauss, const float *record, const int32_t *rect,
+                                int32_t n_channels, const double *bg, int32_t width, int32_t height,
+                                double alpha_clamp, double trans_stop, float *out_img, float *out_t,
+                                int32_t *out_last, int32_t *n_contrib, const int32_t *tile_order,
+                                int32_t *defer, void *stream);
+
 /* Backward tile blend.  d_img H x W x C, d_alpha H x W (storage type).  offsets: the
  * per-Gaussian instance offsets of vegs_bin_count.  Writes per-instance rows [g_mx, g_my,
  * g_ca, g_cb, g_cc, g_alpha, g_ch..., pad] (row stride rec_stride) at the instance's
@@ -215,7 +235,17 @@ typedef struct {
     double log_split_factor; /* log(1.6) */
     int32_t no_weights;      /* 1: pruning off */
     int32_t pad_;
+    /* NULL: prune on sigmoid(raw_weight) < prune_threshold (the reference, train.py:277-280).
+     * Else n float64 per-Gaussian max TF opacities (vegs_tf_max_opacity): prune where
+     * < prune_threshold (BASELINE config 4: "max TF opacity < 0.005"). */
+    const double *prune_opacity;
 } VegsDensify;
+
+/* out[g] = O(sigmoid(raw_value[g])) for the opacity map of tf (init != 0), else
+ * max(out[g], O(...)): called once per training TF, the per-Gaussian max TF opacity of
+ * BASELINE config 4's prune rule (eval_opacity semantics, transfer.py:91-95). */
+int vegs_tf_max_opacity(const double *params, int64_t n, const VegsTF *tf, int32_t init, double *out,
+                        void *stream);
 
 /* stats: n x 5 float64 [sum viewspace_norm, sum position grad (3), count] (DensifyStats).
  * flags / offsets: (n+1) x int4 = (keep, clone, split, split-any); offsets[n] holds the

@@ -589,3 +589,78 @@ def learning_rates(cfg: dict, iteration: int, extent: float = 1.0) -> dict:
     return dict(position=lr_pos, log_scale=cfg["lr_scale"], rotation=cfg["lr_rotation"],
                 raw_value=cfg["lr_value"], raw_weight=0.0 if cfg.get("no_weights") else cfg["lr_weight"],
                 normal=lit, raw_ka=lit, raw_kd=lit, raw_ks=lit, raw_beta=lit)
+
+
+# ----------------------------------------------------------------------------- densify / prune
+
+CLASSES = ("position", "log_scale", "rotation", "raw_value", "raw_weight", "normal", "raw_ka", "raw_kd",
+           "raw_ks", "raw_beta")
+
+
+def tf_max_opacity(raw_value, op_maps):
+    """BASELINE config 4's prune criterion: per Gaussian, the max over the training TFs of
+    the opacity map at the activated value (eval_opacity, transfer.py:91-95).
+    op_maps: list of (ts, values)."""
+    v = np.clip(_sig(np.asarray(raw_value, dtype=np.float64)), 0.0, 1.0)
+    return np.max(np.stack([np.interp(v, ts, vals) for ts, vals in op_maps]), axis=0)
+
+
+def densify_and_prune(p, m, v, grad_accum, pos_accum, count, cfg, extent, rng, position_lr,
+                      prune_opacity=None, max_gaussians=None):
+    """train.py:237-284 on dicts of class arrays (p, m, v), with BASELINE config 4's options:
+    prune_opacity (per-Gaussian max TF opacity) replaces the activated weight in the prune
+    test (train.py:277-280), and max_gaussians caps the count -- when clones and splits
+    would exceed it, this round densifies nothing and only prunes (the build's reconciliation,
+    DESIGN.md).  Returns (p, m, v) of the new set; optimizer rows follow OptimizerState.edit_rows
+    / select_rows (train.py:143-153: kept rows keep their moments, new rows start at zero)."""
+    n = len(p["raw_weight"])
+    cnt = np.maximum(count, 1.0)
+    cand = grad_accum / cnt > cfg["densify_grad_threshold"]
+    max_scale = np.exp(p["log_scale"]).max(axis=1) if n else np.zeros(0)
+    small = cand & (max_scale <= cfg["percent_dense"] * extent)
+    big = cand & ~small
+    if cfg.get("no_weights"):
+        surv_g = np.ones(n, dtype=bool)
+    elif prune_opacity is not None:
+        surv_g = np.asarray(prune_opacity) >= cfg["prune_weight_threshold"]
+    else:
+        surv_g = _sig(p["raw_weight"]) >= cfg["prune_weight_threshold"]
+    if max_gaussians is not None:
+        grow = int(((~big) & surv_g).sum() + (small & surv_g).sum() + 2 * (big & surv_g).sum())
+        if grow > max_gaussians and (small.any() or big.any()):
+            small = np.zeros(n, dtype=bool)
+            big = np.zeros(n, dtype=bool)
+    keep = ~big
+    parts = [{k: p[k][keep] for k in CLASSES}]
+    mparts = [{k: m[k][keep] for k in CLASSES}]
+    vparts = [{k: v[k][keep] for k in CLASSES}]
+    survive = [surv_g[keep]]
+    ci = np.flatnonzero(small)
+    if len(ci):
+        c = {k: p[k][ci].copy() for k in CLASSES}
+        g = pos_accum[ci] / cnt[ci, None]
+        nrm = np.linalg.norm(g, axis=1, keepdims=True)
+        d = np.where(nrm > 0, g / np.maximum(nrm, 1e-30), 0.0)
+        c["position"] = c["position"] - position_lr * d
+        parts.append(c)
+        survive.append(surv_g[ci])
+    si = np.flatnonzero(big)
+    if len(si):
+        for _ in range(2):
+            c = {k: p[k][si].copy() for k in CLASSES}
+            eps = rng.standard_normal(size=(len(si), 3))
+            rot = np.moveaxis(np.array(quat_rot(c["rotation"] / np.linalg.norm(c["rotation"], axis=1,
+                                                                                 keepdims=True))), 2, 0)
+            off = np.einsum("nij,nj->ni", rot, np.exp(c["log_scale"]) * eps)
+            c["position"] = c["position"] + off
+            c["log_scale"] = c["log_scale"] - np.log(1.6)
+            parts.append(c)
+            survive.append(surv_g[si])
+    n_new = sum(len(q["raw_weight"]) for q in parts[1:])
+    zeros = {k: np.zeros((n_new,) + p[k].shape[1:]) for k in CLASSES}
+    out_p = {k: np.concatenate([q[k] for q in parts]) for k in CLASSES}
+    out_m = {k: np.concatenate([mparts[0][k], zeros[k]]) for k in CLASSES}
+    out_v = {k: np.concatenate([vparts[0][k], zeros[k]]) for k in CLASSES}
+    s = np.concatenate(survive)
+    return ({k: a[s] for k, a in out_p.items()}, {k: a[s] for k, a in out_m.items()},
+            {k: a[s] for k, a in out_v.items()})

@@ -44,7 +44,7 @@ class VegsSplatTable(ctypes.Structure):
 class VegsDensify(ctypes.Structure):
     _fields_ = [("grad_threshold", c_double), ("percent_dense", c_double), ("scene_extent", c_double),
                 ("prune_threshold", c_double), ("position_lr", c_double), ("log_split_factor", c_double),
-                ("no_weights", c_int32), ("pad_", c_int32)]
+                ("no_weights", c_int32), ("pad_", c_int32), ("prune_opacity", c_void_p)]
 
 
 P = c_void_p
@@ -59,12 +59,15 @@ _SIGS = {
                       POINTER(c_size_t), P],
     "vegs_composite_forward": [P, P, P, P, P, c_int32, c_int32, P, c_int32, c_int32, c_double, c_double,
                                P, P, P, P, P, P],
+    "vegs_composite_forward_fast": [P, P, P, P, P, c_int32, P, c_int32, c_int32, c_double, c_double, P, P, P, P,
+                                    P, P, P],
     "vegs_composite_backward": [P, P, P, P, P, P, c_int32, c_int32, P, c_int32, c_int32, c_double, P, P,
                                 P, P, P, P, c_int64, P, P],
     "vegs_preprocess_backward": [P, c_int64, POINTER(VegsCamera), POINTER(VegsTF), POINTER(VegsSettings),
                                  c_int32, c_int32, P, P, P, c_double, c_int32, P, P, P, P, P, P,
                                  POINTER(c_size_t), P],
     "vegs_densify_count": [P, c_int64, P, POINTER(VegsDensify), P, P, P, POINTER(c_size_t), P],
+    "vegs_tf_max_opacity": [P, c_int64, POINTER(VegsTF), c_int32, P, P],
     "vegs_densify_apply": [P, P, P, c_int64, P, POINTER(VegsDensify), P, P, P, c_int64, P, P, P, P],
     "vegs_blend_forward": [P, P, c_int64, c_int64, c_int64, P, P, P, P, P, P, c_int32, c_int32, P, c_int64,
                            c_int64, c_double, c_double, P, P, P, P, P],

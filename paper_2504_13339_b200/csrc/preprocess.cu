@@ -275,6 +275,20 @@ struct Int4Sum {
     }
 };
 
+// Max over transfer functions of the opacity map at each Gaussian's value (BASELINE config
+// 4's prune criterion "max TF opacity < 0.005"): out[g] = max(out[g], O_tf(sigmoid(raw_value)))
+// (init: out[g] = O_tf(...)), np.interp semantics as eval_opacity (transfer.py:91-95).
+__global__ void tf_max_opacity_kernel(const double *params, int64_t n, VegsTF tf, int init, double *out) {
+    extern __shared__ double s_tf[];
+    for (int i = threadIdx.x; i < 2 * tf.n_opacity; i += blockDim.x) s_tf[i] = tf.blob[i];
+    __syncthreads();
+    const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (g >= n) return;
+    const ParamView P(params, n);
+    const double o = tf_interp(s_tf, s_tf + tf.n_opacity, tf.n_opacity, clip01(sigmoid(P.raw_value[g])));
+    out[g] = init ? o : fmax(out[g], o);
+}
+
 __device__ __forceinline__ void densify_flags(const ParamView &P, int64_t g, const double *stats,
                                               const VegsDensify &dp, bool &small, bool &big, bool &survive) {
     const double cnt = fmax(stats[5 * g + 4], 1.0);
@@ -284,7 +298,11 @@ __device__ __forceinline__ void densify_flags(const ParamView &P, int64_t g, con
     ms = fmax(ms, exp(P.log_scale[3 * g + 2]));
     small = cand && ms <= dp.percent_dense * dp.scene_extent;
     big = cand && !small;
-    survive = dp.no_weights || sigmoid(P.raw_weight[g]) >= dp.prune_threshold;
+    // prune rule: the reference's activated weight (train.py:277-280), or BASELINE config 4's
+    // max TF opacity over the training TFs (dp.prune_opacity, from vegs_tf_max_opacity)
+    survive = dp.no_weights ||
+              (dp.prune_opacity ? dp.prune_opacity[g] >= dp.prune_threshold
+                                : sigmoid(P.raw_weight[g]) >= dp.prune_threshold);
 }
 
 __global__ void densify_classify_kernel(const double *params, int64_t n, const double *stats, VegsDensify dp,
@@ -410,6 +428,17 @@ extern "C" int vegs_densify_count(const double *params, int64_t n, const double 
     VEGS_CHECK_LAUNCH();
     VEGS_CUDA(cub::DeviceScan::ExclusiveScan(ws, scan_bytes, (int4 *)flags, (int4 *)offsets, Int4Sum(),
                                              make_int4(0, 0, 0, 0), n + 1, s));
+    return VEGS_OK;
+}
+
+extern "C" int vegs_tf_max_opacity(const double *params, int64_t n, const VegsTF *tf, int32_t init, double *out,
+                                   void *stream) {
+    if (!tf_ok(tf) || (n > 0 && (!params || !out))) return VEGS_ERR_ARG;
+    if (n == 0) return VEGS_OK;
+    const size_t smem = sizeof(double) * 2 * (size_t)tf->n_opacity;
+    VEGS_CUDA(cudaFuncSetAttribute(tf_max_opacity_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    tf_max_opacity_kernel<<<(int)((n + 255) / 256), 256, smem, (cudaStream_t)stream>>>(params, n, *tf, init, out);
+    VEGS_CHECK_LAUNCH();
     return VEGS_OK;
 }
 

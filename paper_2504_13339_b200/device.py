@@ -43,6 +43,7 @@ LAUNCHES = {
                                   # tile weights + single-tile CUB sort (heaviest-first tile order); +1 (order /
                                   # inst_pid) on the API path.  Radix path (> 12288 tiles): 19.
     "vegs_composite_forward": 1,
+    "vegs_composite_forward_fast": 2,  # blend + float64 fix-up of the undecidable pixels (+ a 4-byte memset)
     "vegs_composite_backward": 1,
     "vegs_preprocess_backward": 2,  # row reduction + chain
     "vegs_loss_l1_ssim": 2,
@@ -207,6 +208,12 @@ class Frame:
     n_contrib: torch.Tensor | None
     api: dict = field(default_factory=dict)
     visited: torch.Tensor | None = None  # per-instance bitmask of the latest backward_rows
+    defer: torch.Tensor | None = None  # fast-T forward: [count, pixels re-blended in float64]
+
+    @property
+    def n_deferred(self) -> int:
+        """Pixels the fast-T forward handed to its float64 fix-up pass (host sync)."""
+        return 0 if self.defer is None else int(self.defer[0].item())
 
     @property
     def real(self):
@@ -222,7 +229,7 @@ class Rasterizer:
     may outlive later renders)."""
 
     def __init__(self, settings: RasterSettings = DEFAULT_SETTINGS, n_channels: int = 3,
-                 store_f64: bool = False, pooled: bool = True):
+                 store_f64: bool = False, pooled: bool = True, fast_t: bool = False):
         if n_channels not in (3, 11):
             raise ValueError("n_channels must be 3 (rgb) or 11 (rgb + aux planes)")
         self.device = require_cuda()
@@ -237,6 +244,9 @@ class Rasterizer:
         self.launches = 0  # kernels launched by this rasteriser (see LAUNCHES)
         self.last_counts = (0, 0)  # (kept splats, tile instances) of the latest forward
         self.contrib_counts = True  # per-pixel contributor counts (the trainer turns them off)
+        # float32 blends: carry T in float32 with exact decisions (vegs_composite_forward_fast)
+        # instead of the float64 chain that reproduces the reference's T bit for bit
+        self.fast_t = fast_t
 
     def _run(self, name: str, *args) -> None:
         if self.timer is not None:
@@ -353,16 +363,24 @@ class Rasterizer:
         out_last = A.get("out_last", hw, torch.int32)
         n_contrib = A.get("n_contrib", hw, torch.int32) if self.contrib_counts else None
         bg = (ctypes.c_double * 3)(*[float(x) for x in background])
-        self._run("vegs_composite_forward", _p(tile_start), _p(tile_end), _p(sorted_gauss), _p(record), _p(rect),
-             self.n_ch, int(self.store_f64), bg, width, height, float(self.settings.alpha_clamp),
-             float(self.settings.transmittance_stop), _p(out_img), _p(out_t), _p(out_last), _p(n_contrib),
-             _p(tile_order), s)
+        defer = None
+        if self.fast_t and not self.store_f64:
+            defer = A.get("defer", hw + 1, torch.int32)
+            self._run("vegs_composite_forward_fast", _p(tile_start), _p(tile_end), _p(sorted_gauss), _p(record),
+                      _p(rect), self.n_ch, bg, width, height, float(self.settings.alpha_clamp),
+                      float(self.settings.transmittance_stop), _p(out_img), _p(out_t), _p(out_last), _p(n_contrib),
+                      _p(tile_order), _p(defer), s)
+        else:
+            self._run("vegs_composite_forward", _p(tile_start), _p(tile_end), _p(sorted_gauss), _p(record), _p(rect),
+                      self.n_ch, int(self.store_f64), bg, width, height, float(self.settings.alpha_clamp),
+                      float(self.settings.transmittance_stop), _p(out_img), _p(out_t), _p(out_last), _p(n_contrib),
+                      _p(tile_order), s)
         return Frame(n=n, n_ch=self.n_ch, store_f64=self.store_f64, width=width, height=height, cam=cs, tf=tf,
                      settings=self.st, bg=bg, params=params, record=record, rect=rect, tiles=tiles,
                      depth_key=depth_key, offsets=offsets, kept_idx=kept_idx, n_kept=n_kept, n_inst=n_inst,
                      sorted_gauss=sorted_gauss, inst_pid=inst_pid, order=order, tile_start=tile_start,
                      tile_end=tile_end, tile_order=tile_order, out_img=out_img, out_t=out_t, out_last=out_last,
-                     n_contrib=n_contrib, api=api)
+                     n_contrib=n_contrib, api=api, defer=defer)
 
     # -- backward -------------------------------------------------------------------
     def backward_rows(self, fr: Frame, d_img: torch.Tensor, d_alpha: torch.Tensor | None = None) -> torch.Tensor:
@@ -474,11 +492,12 @@ class RenderPipeline:
     count, so the small per-view kernels overlap the previous view's compositing.
     Output frames are only valid until the lane that produced them is reused."""
 
-    def __init__(self, settings: RasterSettings = DEFAULT_SETTINGS, n_channels: int = 3, lanes: int = 4):
+    def __init__(self, settings: RasterSettings = DEFAULT_SETTINGS, n_channels: int = 3, lanes: int = 4,
+                 fast_t: bool = True):
         dev = self.device = require_cuda()
         main = torch.cuda.current_stream(dev)
-        self.lanes = [(main if i == 0 else torch.cuda.Stream(dev), Rasterizer(settings, n_channels, pooled=True))
-                      for i in range(max(1, lanes))]
+        self.lanes = [(main if i == 0 else torch.cuda.Stream(dev),
+                       Rasterizer(settings, n_channels, pooled=True, fast_t=fast_t)) for i in range(max(1, lanes))]
         for _, rz in self.lanes:
             rz.contrib_counts = False  # images only
 

@@ -169,7 +169,7 @@ class _Lane:
         from .device import LossKernel
 
         self.stream = stream
-        self.rz = Rasterizer(tr.settings, 11 if tr.with_aux else 3, store_f64=False, pooled=True)
+        self.rz = Rasterizer(tr.settings, 11 if tr.with_aux else 3, store_f64=False, pooled=True, fast_t=tr.fast_t)
         self.rz.contrib_counts = False  # nobody reads them in training
         self.loss = LossKernel(tr.device)
         self.loss_launches = 0
@@ -194,8 +194,11 @@ class Trainer:
 
     def __init__(self, gs: GaussianSet, config: TrainConfig, settings: RasterSettings = DEFAULT_SETTINGS,
                  background=(1.0, 1.0, 1.0), l1_weight: float | None = None, group=None, with_aux: bool = False,
-                 lanes: int = 4):
+                 lanes: int = 4, fast_t: bool = True):
         self.device = require_cuda()
+        # fast_t: the forward carries T in float32 with every skip / clamp / termination
+        # decision exact (vegs_composite_forward_fast); False: the float64 chain
+        self.fast_t = fast_t
         self.n = len(gs)
         self.config = config
         self.settings = settings
@@ -381,16 +384,22 @@ class Trainer:
                 lane.dstats.zero_()
         return self.densify_stats
 
-    def densify_and_prune(self, scene_extent: float, rng: np.random.Generator, position_lr: float) -> int:
+    def densify_and_prune(self, scene_extent: float, rng: np.random.Generator, position_lr: float,
+                          prune_tfs=None, max_gaussians: int | None = None) -> int:
         """Device densify/prune of the resident set; the step's buffers are resized and
         the densification statistics reset.  With world_size > 1 the statistics are
-        all-reduced first so every replica makes the same decision.  Returns the new n."""
+        all-reduced first so every replica makes the same decision.  Returns the new n.
+
+        ``prune_tfs`` (DeviceTFs) / ``max_gaussians``: BASELINE config 4's rule -- prune on
+        the max opacity over these TFs instead of the activated weight, and cap the count
+        (see ``densify_device``).  Defaults: the reference's rule, no cap."""
         if self.densify_stats is None:
             raise RuntimeError("call track_densify() before training steps to collect statistics")
         self.gather_densify_stats()
         allreduce_gradients(self.densify_stats, self.group)
+        mo = tf_max_opacity(self.params, self.n, prune_tfs) if prune_tfs else None
         p, m, v, n_out = densify_device(self.params, self.m, self.v, self.n, self.densify_stats, self.config,
-                                        scene_extent, rng, position_lr)
+                                        scene_extent, rng, position_lr, mo, max_gaussians)
         self.params, self.m, self.v, self.n = p.clone(), m.clone(), v.clone(), n_out
         self.grads = torch.zeros_like(self.params)
         self.densify_stats = torch.zeros(self.n * 5, dtype=torch.float64, device=self.device)
@@ -416,35 +425,65 @@ SPLIT_SCALE_FACTOR = 1.6
 WEIGHT_RESET_VALUE = 0.01
 
 
-def _densify_struct(config: TrainConfig, scene_extent: float, position_lr: float):
+def _densify_struct(config: TrainConfig, scene_extent: float, position_lr: float, prune_opacity=None):
     from ._lib import VegsDensify
 
     return VegsDensify(config.densify_grad_threshold, config.percent_dense, float(scene_extent),
                        config.prune_weight_threshold, float(position_lr), math.log(SPLIT_SCALE_FACTOR),
-                       int(config.no_weights), 0)
+                       int(config.no_weights), 0, None if prune_opacity is None else prune_opacity.data_ptr())
+
+
+def tf_max_opacity(params: torch.Tensor, n: int, tfs) -> torch.Tensor:
+    """Per-Gaussian max over ``tfs`` (DeviceTF) of the opacity map at sigmoid(raw_value):
+    BASELINE config 4's prune criterion (vegs_tf_max_opacity, one launch per TF)."""
+    import ctypes
+
+    from . import _lib
+    from .device import _p, _stream
+
+    if not tfs:
+        raise ValueError("need at least one transfer function")
+    out = torch.empty(max(n, 1), dtype=torch.float64, device=params.device)
+    for k, tf in enumerate(tfs):
+        _lib.call("vegs_tf_max_opacity", _p(params), n, ctypes.byref(tf.struct), int(k == 0), _p(out), _stream())
+    return out[:n]
 
 
 def densify_device(params: torch.Tensor, m: torch.Tensor, v: torch.Tensor, n: int, stats: torch.Tensor,
-                   config: TrainConfig, scene_extent: float, rng: np.random.Generator, position_lr: float):
+                   config: TrainConfig, scene_extent: float, rng: np.random.Generator, position_lr: float,
+                   prune_opacity: torch.Tensor | None = None, max_gaussians: int | None = None):
     """Clone / split / prune on device buffers; returns (params, m, v, n_out).
 
     The split offsets are drawn on the host from ``rng`` exactly as the reference does
-    (two rounds of ``standard_normal((n_split, 3))``), so a seeded run reproduces it."""
+    (two rounds of ``standard_normal((n_split, 3))``), so a seeded run reproduces it.
+
+    ``prune_opacity`` (n float64, see ``tf_max_opacity``) switches the prune rule from the
+    reference's activated weight (train.py:277-280) to BASELINE config 4's "max TF opacity
+    < prune_weight_threshold".  ``max_gaussians`` is BASELINE config 4's cap: when clones
+    and splits would take the set above it, this round densifies nothing (pruning still
+    runs), so the set never grows past the cap by densification."""
     import ctypes
 
     from . import _lib
     from .device import _p, _stream
 
     dev = params.device
-    dp = _densify_struct(config, scene_extent, position_lr)
+    dp = _densify_struct(config, scene_extent, position_lr, prune_opacity)
     flags = torch.empty(4 * (n + 1), dtype=torch.int32, device=dev)
     offs = torch.empty_like(flags)
     nbytes = _lib.size_query("vegs_densify_count", _p(params), n, _p(stats), ctypes.byref(dp), _p(flags), _p(offs),
                              tail=(_stream(),))
     ws = torch.empty(max(nbytes, 1), dtype=torch.uint8, device=dev)
-    _lib.call("vegs_densify_count", _p(params), n, _p(stats), ctypes.byref(dp), _p(flags), _p(offs), _p(ws),
-              ctypes.byref(ctypes.c_size_t(nbytes)), _stream())
-    keep, clone, split, n_split = (int(x) for x in offs[4 * n:4 * n + 4].tolist())
+
+    def count():
+        _lib.call("vegs_densify_count", _p(params), n, _p(stats), ctypes.byref(dp), _p(flags), _p(offs), _p(ws),
+                  ctypes.byref(ctypes.c_size_t(nbytes)), _stream())
+        return [int(x) for x in offs[4 * n:4 * n + 4].tolist()]
+
+    keep, clone, split, n_split = count()
+    if max_gaussians is not None and keep + clone + 2 * split > max_gaussians and clone + split > 0:
+        dp.grad_threshold = math.inf  # the cap: no densification this round
+        keep, clone, split, n_split = count()
     if n_split:
         eps_h = np.concatenate([rng.standard_normal(size=(n_split, 3)) for _ in range(2)])
     else:

@@ -1,5 +1,5 @@
 """Quick timing of every C-ABI call of one config-2 view (CUDA events around each call on a
-single stream, forward + backward over 4 views): python scripts/time_kernels.py [reps] [channels] [f64]"""
+single stream, forward + backward over 4 views): python scripts/time_kernels.py [reps] [channels] [f64|fast]"""
 import sys
 from collections import defaultdict
 from pathlib import Path
@@ -16,9 +16,10 @@ def main():
     reps = int(sys.argv[1]) if len(sys.argv) > 1 else 10
     n_ch = int(sys.argv[2]) if len(sys.argv) > 2 else 3
     f64 = len(sys.argv) > 3 and sys.argv[3] == "f64"  # the float64 blend (reference default dtype)
+    fast = len(sys.argv) > 3 and sys.argv[3] == "fast"  # float32-T forward (training path)
     gs, truth, tf, cams = scenes.config_scene("c2")
     dtf = DeviceTF(tf)
-    rz = Rasterizer(n_channels=n_ch, store_f64=f64)
+    rz = Rasterizer(n_channels=n_ch, store_f64=f64, fast_t=fast)
     params = torch.from_numpy(gs.pack()).cuda()
     grads = torch.zeros_like(params)
     times = defaultdict(list)
@@ -45,6 +46,8 @@ def main():
                 loss.timer = rz.timer
                 loss(fr.out_img.view(1024, 1024, 3), target, 0.8, 0.2, d_loss, sums)
             rz.backward(fr, d_img, None, grads, accumulate=True)
+            if fast and r == reps + 1:
+                print("deferred pixels", fr.n_deferred)
     torch.cuda.synchronize()
     for k, v in times.items():
         ms = [a.elapsed_time(b) for a, b in v]

@@ -130,15 +130,16 @@ def test_c3_frame_through_render_pipeline_vs_reference():
     got = {}
 
     def keep(i, fr):
-        got[i] = (fr.out_img.view(cam.height, cam.width, 3).clone(), fr.out_t.view(cam.height, cam.width).clone())
+        got[i] = (fr.out_img.view(-1, 3).clone(), fr.out_t.clone(), fr.out_last.clone())
 
-    pipe = RenderPipeline(lanes=3)
+    pipe = RenderPipeline(lanes=3)  # fast-T forward (float32 chain, exact decisions)
     pipe.render(params, len(gs), [(cam, other), (cam, dtf), (cam, other), (cam, dtf)], on_frame=keep)
     torch.cuda.synchronize()
+    pix = d["pix"]
     for i in (1, 3):
-        rgb, t = (x.cpu().numpy() for x in got[i])
-        assert np.array_equal(digest(t, np.float32), d["out_t_sha"]), i
-        assert img_close(rgb.reshape(-1, 3)[d["pix"]], d["pix_rgb"]), i
+        rgb, t, last = (x.cpu().numpy() for x in got[i])
+        assert np.array_equal(digest(last.astype(np.int64), np.int64), d["out_last_sha"]), i
+        assert img_close(t[pix], d["pix_t"]) and img_close(rgb[pix], d["pix_rgb"]), i
 
 
 @pytest.mark.parametrize("lanes", [1, 2, 3, 4])
@@ -152,7 +153,7 @@ def test_render_pipeline_frames_equal_single_stream(lanes):
     tfs = [DeviceTF(scenes.random_tf(1000 + k)) for k in range(3)]
     items = [(cams[i % len(cams)], tfs[i % len(tfs)]) for i in range(7)]
     ref = []
-    rz = Rasterizer(pooled=False)
+    rz = Rasterizer(pooled=False, fast_t=True)  # the pipeline's forward, single stream
     for cam, tf in items:
         fr = rz.forward(params, len(gs), tf, cam)
         ref.append((fr.out_img.clone(), fr.out_t.clone(), fr.out_last.clone()))
@@ -301,3 +302,124 @@ def test_adam_lane_sum_equals_eager_adds():
         adam_step_device(None, g_sum, None, None, n, None, 1.0, 1, None, [x for x in gs[1:k]])
         assert torch.equal(g_sum, g_eager), k
     assert not bad.any()
+
+
+# -- the fast-T forward (vegs_composite_forward_fast): float32 chain, exact decisions ------
+
+FAST_CASES = [("c0_f32", False), ("dense_f32", False), ("c0_aux_f32", True)]
+
+
+@pytest.mark.parametrize("name,aux", FAST_CASES, ids=[c[0] for c in FAST_CASES])
+def test_fast_t_forward_vs_reference_goldens(name, aux):
+    """The training / render path's forward against the reference fixtures: last
+    contributor and contributor count bit-exact, T and the planes within the image bar."""
+    d = G.load(name)
+    params = torch.from_numpy(G.gs_of(d).pack()).cuda()
+    cam = G.cam_of(d["cam"])
+    rz = Rasterizer(n_channels=11 if aux else 3, pooled=False, fast_t=True)
+    fr = rz.forward(params, len(d["gs_position"]), DeviceTF(G.tf_of(d)), cam, tuple(d["bg"]))
+    h, w = cam.height, cam.width
+    assert np.array_equal(fr.out_last.cpu().numpy().reshape(h, w), d["out_last"])
+    assert np.array_equal(fr.n_contrib.cpu().numpy().reshape(h, w), d["n_contrib"])
+    assert img_close(fr.out_t.cpu().numpy().reshape(h, w), d["out_t"])
+    assert img_close(fr.out_img.view(h, w, -1)[:, :, :3].cpu().numpy(), d["rgb"])
+
+
+def test_fast_t_forward_equals_exact_forward_decisions():
+    """Fast vs float64-chain forward on a 1080p blob scene: every integer decision
+    equal, T within the bound the kernel tracks, few pixels deferred to the fix-up."""
+    gs = scenes.blob_gaussians(200_000, seed=1)
+    params = torch.from_numpy(gs.pack()).cuda()
+    cam = scenes.orbit_cameras(1, 5, 1920, 1080)[0]
+    tf = DeviceTF(scenes.random_tf(1000))
+    ex = Rasterizer(pooled=False).forward(params, len(gs), tf, cam)
+    fa = Rasterizer(pooled=False, fast_t=True).forward(params, len(gs), tf, cam)
+    assert torch.equal(fa.out_last, ex.out_last)
+    assert torch.equal(fa.n_contrib, ex.n_contrib)
+    rel = ((fa.out_t.double() - ex.out_t.double()).abs() / ex.out_t.double().clamp(min=1e-3)).max().item()
+    assert rel <= 1e-4, rel
+    assert img_close(fa.out_img.cpu().numpy(), ex.out_img.cpu().numpy())
+    assert fa.n_deferred < 0.01 * cam.width * cam.height
+
+
+def test_fast_t_fixup_is_exact_when_every_pixel_is_deferred(monkeypatch):
+    """Forcing every terminating test to be undecidable (VEGS_FAST_T_DEFER_ALL) sends those
+    pixels through the float64 fix-up: the frame then equals the float64-chain forward
+    bit for bit (T included) wherever the fix-up ran."""
+    monkeypatch.setenv("VEGS_FAST_T_DEFER_ALL", "1")
+    d = G.load("dense_f32")
+    params = torch.from_numpy(G.gs_of(d).pack()).cuda()
+    cam = G.cam_of(d["cam"])
+    tf = DeviceTF(G.tf_of(d))
+    fa = Rasterizer(pooled=False, fast_t=True).forward(params, len(d["gs_position"]), tf, cam, tuple(d["bg"]))
+    assert fa.n_deferred > 0
+    h, w = cam.height, cam.width
+    pix = fa.defer[1:1 + fa.n_deferred].cpu().numpy()
+    assert np.array_equal(fa.out_last.cpu().numpy(), d["out_last"].reshape(-1))
+    assert np.array_equal(fa.n_contrib.cpu().numpy(), d["n_contrib"].reshape(-1))
+    assert np.array_equal(fa.out_t.cpu().numpy()[pix], d["out_t"].reshape(-1)[pix])
+
+
+@pytest.mark.slow
+def test_c2_fast_t_forward_vs_reference(c2_ref):
+    """The benchmark's own forward (fast T) on the pinned c2 view: last contributor and
+    contributor count digests equal the reference's; sampled T / rgb within the bar."""
+    d, gs, cam, img, st = c2_ref
+    params = torch.from_numpy(gs.pack()).cuda()
+    fr = Rasterizer(pooled=False, fast_t=True).forward(params, len(gs), DeviceTF(scenes.config_scene("c2")[2]), cam)
+    last = fr.out_last.cpu().numpy().astype(np.int64)
+    ncon = fr.n_contrib.cpu().numpy()
+    pix = d["pix"]
+    assert np.array_equal(last[pix], d["pix_last"]) and np.array_equal(ncon[pix], d["pix_ncon"])
+    assert np.array_equal(digest(last, np.int64), d["out_last_sha"])
+    assert np.array_equal(digest(ncon, np.int32), d["n_contrib_sha"])
+    assert img_close(fr.out_t.cpu().numpy()[pix], d["pix_t"])
+    assert img_close(fr.out_img.view(-1, 3).cpu().numpy()[pix], d["pix_rgb"])
+    assert fr.n_deferred < 0.01 * cam.width * cam.height
+
+
+# -- BASELINE config 4's densify rule (max TF opacity prune, count cap) vs the oracle --------
+
+@pytest.mark.parametrize("cap", [None, "tight"])
+def test_densify_config4_rule_matches_oracle(cap):
+    from paper_2504_13339_b200.model import GaussianSet
+    from paper_2504_13339_b200.train import densify_device, tf_max_opacity
+
+    d = G.load("densify")
+    gs = GaussianSet(**{k: d["in_" + k].copy() for k in PARAM_CLASSES})
+    n = len(gs)
+    tfs = [scenes.range_tf(500 + k, k / 4, (k + 1) / 4) for k in range(4)]
+    params = torch.from_numpy(gs.pack()).cuda()
+
+    def flat(prefix):
+        return torch.from_numpy(np.concatenate([d[prefix + k].ravel() for k in PARAM_CLASSES])).cuda()
+
+    m, v = flat("in_m_"), flat("in_v_")
+    stats = torch.from_numpy(np.concatenate([d["stats_grad"][:, None], d["stats_pos"], d["stats_count"][:, None]],
+                                            axis=1).copy()).cuda()
+    mo = tf_max_opacity(params, n, [DeviceTF(t) for t in tfs])
+    mo_ref = O.tf_max_opacity(d["in_raw_value"], [(t.opacity.ts, t.opacity.values) for t in tfs])
+    assert np.array_equal(mo.cpu().numpy(), mo_ref)
+    cfg = TrainConfig(iterations=100)
+    ocfg = dict(densify_grad_threshold=cfg.densify_grad_threshold, percent_dense=cfg.percent_dense,
+                prune_weight_threshold=cfg.prune_weight_threshold, no_weights=False)
+    p_in = {k: d["in_" + k].copy() for k in O.CLASSES}
+    m_in = {k: d["in_m_" + k].copy() for k in O.CLASSES}
+    v_in = {k: d["in_v_" + k].copy() for k in O.CLASSES}
+    args = (d["stats_grad"], d["stats_pos"], d["stats_count"], ocfg, 3.0)
+    cap_n = None
+    if cap:
+        free, _, _ = O.densify_and_prune(p_in, m_in, v_in, *args, np.random.default_rng(7), 1e-3, mo_ref)
+        cap_n = len(free["raw_weight"]) - 1
+    op, om, ov = O.densify_and_prune(p_in, m_in, v_in, *args, np.random.default_rng(7), 1e-3, mo_ref, cap_n)
+    p, mm, vv, n_out = densify_device(params, m, v, n, stats, cfg, 3.0, np.random.default_rng(7), 1e-3, mo, cap_n)
+    assert n_out == len(op["raw_weight"])
+    if cap:
+        assert n_out <= cap_n
+    gp = GaussianSet.unpack(p.cpu().numpy(), n_out)
+    gm = GaussianSet.unpack(mm.cpu().numpy(), n_out)
+    gv = GaussianSet.unpack(vv.cpu().numpy(), n_out)
+    for k in PARAM_CLASSES:
+        ref = op[k]
+        assert np.abs(getattr(gp, k) - ref).max() <= 1e-12 * max(np.abs(ref).max(), 1.0), k
+        assert np.array_equal(getattr(gm, k), om[k]) and np.array_equal(getattr(gv, k), ov[k]), k

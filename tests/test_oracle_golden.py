@@ -127,3 +127,48 @@ def test_adam_three_steps():
     for k in O.GRAD_CLASSES:
         assert np.array_equal(params[k], d["out_" + k]), k
         assert np.array_equal(m[k], d["m_" + k]) and np.array_equal(v[k], d["v_" + k])
+
+
+DENSIFY_CFG = dict(densify_grad_threshold=2e-4, percent_dense=0.01, prune_weight_threshold=0.005, no_weights=False)
+
+
+def _densify_inputs(d):
+    p = {k: d["in_" + k].copy() for k in O.CLASSES}
+    m = {k: d["in_m_" + k].copy() for k in O.CLASSES}
+    v = {k: d["in_v_" + k].copy() for k in O.CLASSES}
+    return p, m, v
+
+
+def test_densify_restatement_matches_reference():
+    """The oracle's densify/prune (train.py:237-284) reproduces the reference's fixture,
+    rng draws included; its config-4 options default off."""
+    d = G.load("densify")
+    p, m, v = _densify_inputs(d)
+    op, om, ov = O.densify_and_prune(p, m, v, d["stats_grad"], d["stats_pos"], d["stats_count"], DENSIFY_CFG, 3.0,
+                                     np.random.default_rng(7), 1e-3)
+    for k in O.CLASSES:
+        ref = d["out_" + k]
+        assert op[k].shape == ref.shape, k
+        assert np.abs(op[k] - ref).max() <= 1e-12 * max(np.abs(ref).max(), 1.0), k
+        assert np.array_equal(om[k], d["out_m_" + k]) and np.array_equal(ov[k], d["out_v_" + k]), k
+
+
+def test_densify_config4_rule_and_cap_on_the_oracle():
+    """BASELINE config 4's options: the max-TF-opacity prune keeps exactly the Gaussians
+    whose best TF opacity reaches the threshold (children inherit it); the cap stops
+    densification when it would be exceeded and leaves pruning on."""
+    d = G.load("densify")
+    p, m, v = _densify_inputs(d)
+    from paper_2504_13339_b200 import scenes
+
+    tfs = [scenes.range_tf(500 + k, k / 4, (k + 1) / 4) for k in range(4)]
+    maps = [(tf.opacity.ts, tf.opacity.values) for tf in tfs]
+    mo = O.tf_max_opacity(p["raw_value"], maps)
+    args = (d["stats_grad"], d["stats_pos"], d["stats_count"], DENSIFY_CFG, 3.0)
+    op, _, _ = O.densify_and_prune(p, m, v, *args, np.random.default_rng(7), 1e-3, prune_opacity=mo)
+    p0, _, _ = O.densify_and_prune(p, m, v, *args, np.random.default_rng(7), 1e-3, prune_opacity=np.ones(600))
+    assert len(op["raw_weight"]) < len(p0["raw_weight"])  # some Gaussians fall below 0.005 on every TF
+    capped, _, _ = O.densify_and_prune(p, m, v, *args, np.random.default_rng(7), 1e-3, prune_opacity=mo,
+                                       max_gaussians=len(op["raw_weight"]) - 1)
+    n_surv = int((mo >= 0.005).sum())
+    assert len(capped["raw_weight"]) == n_surv  # no clones / splits, pruning applied
