@@ -63,7 +63,7 @@ def parse():
                     help="--impl reference: stop timing further views of the step after this many seconds")
     ap.add_argument("--no-sweep", action="store_true", help="skip the config-3 TF-sweep render measurement")
     ap.add_argument("--no-c4", action="store_true", help="skip the config-4 densify/prune training measurement")
-    ap.add_argument("--c4-steps", type=int, default=3)
+    ap.add_argument("--c4-steps", type=int, default=20)
     ap.add_argument("--sweep-frames", type=int, default=2)
     ap.add_argument("--lanes", type=int, default=4, help="CUDA-stream lanes of the view pipeline")
     ap.add_argument("--backend", choices=("nccl", "gloo"), default="nccl",
@@ -517,7 +517,10 @@ def run_c4(args, dev, rank, world) -> dict:
         tr.step(views_for(s + 1), total_views=len(cams))
     e1.record()
     n_before = tr.n
-    n_after = tr.densify_and_prune(scene_extent=1.0, rng=np.random.default_rng(7), position_lr=1.6e-4)
+    # BASELINE config 4's rule: prune on the max opacity over the 16 training TFs (< 0.005),
+    # densification capped at 3M Gaussians
+    n_after = tr.densify_and_prune(scene_extent=1.0, rng=np.random.default_rng(7), position_lr=1.6e-4,
+                                   prune_tfs=tfs, max_gaussians=3_000_000)
     e2.record()
     torch.cuda.synchronize()
     step_ms, dens_ms = e0.elapsed_time(e1) / steps, e1.elapsed_time(e2)
@@ -527,7 +530,8 @@ def run_c4(args, dev, rank, world) -> dict:
         step_ms, dens_ms = (float(x) for x in t.tolist())
     return {"workload": "c4: 200k learned Gaussians, targets from a 2M-Gaussian 64-blob set, 64 views/step at "
                         "800x800 sharded across ranks, 16 TFs over disjoint scalar ranges cycled per step, "
-                        "densify/prune every 100 steps (amortised)",
+                        "densify/prune every 100 steps (amortised; clone/split on view-space gradient > 2e-4, "
+                        "prune on max TF opacity < 0.005 over the 16 TFs, capped at 3M)",
             "steps_per_s": 1000.0 / step_ms, "ms_per_step": step_ms, "densify_ms": dens_ms,
             "steps_per_s_amortised": 1000.0 / (step_ms + dens_ms / 100.0), "n_before": n_before,
             "n_after": n_after, "timed_steps": steps}

@@ -493,7 +493,7 @@ class RenderPipeline:
     Output frames are only valid until the lane that produced them is reused."""
 
     def __init__(self, settings: RasterSettings = DEFAULT_SETTINGS, n_channels: int = 3, lanes: int = 4,
-                 fast_t: bool = True):
+                 fast_t: bool = False):
         dev = self.device = require_cuda()
         main = torch.cuda.current_stream(dev)
         self.lanes = [(main if i == 0 else torch.cuda.Stream(dev),

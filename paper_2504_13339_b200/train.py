@@ -194,10 +194,11 @@ class Trainer:
 
     def __init__(self, gs: GaussianSet, config: TrainConfig, settings: RasterSettings = DEFAULT_SETTINGS,
                  background=(1.0, 1.0, 1.0), l1_weight: float | None = None, group=None, with_aux: bool = False,
-                 lanes: int = 4, fast_t: bool = True):
+                 lanes: int = 4, fast_t: bool = False):
         self.device = require_cuda()
         # fast_t: the forward carries T in float32 with every skip / clamp / termination
-        # decision exact (vegs_composite_forward_fast); False: the float64 chain
+        # decision exact (vegs_composite_forward_fast).  Default: the float64 chain, which
+        # also reproduces T bit for bit and measured as fast (A/B)
         self.fast_t = fast_t
         self.n = len(gs)
         self.config = config
