@@ -63,6 +63,8 @@ def parse():
                     help="--impl reference: stop timing further views of the step after this many seconds")
     ap.add_argument("--no-sweep", action="store_true", help="skip the config-3 TF-sweep render measurement")
     ap.add_argument("--no-c4", action="store_true", help="skip the config-4 densify/prune training measurement")
+    ap.add_argument("--no-api", action="store_true", help="skip the numpy drop-in API timing")
+    ap.add_argument("--api-views", type=int, default=3)
     ap.add_argument("--c4-steps", type=int, default=20)
     ap.add_argument("--sweep-frames", type=int, default=2)
     ap.add_argument("--lanes", type=int, default=4, help="CUDA-stream lanes of the view pipeline")
@@ -184,6 +186,50 @@ def stage_bytes(name: str, n: int, n_kept: int, n_inst: int, pixels: int) -> flo
     if name == "vegs_preprocess_backward":  # params in, gradients read+written, row sums
         return float(152 * n + 304 * n + 72 * n_kept)
     return None
+
+
+def composite_roofline(ksum: dict, pixels: int, ncu_key: str, ncu_file: str = "ncu_composite.json") -> dict | None:
+    """Roofline of the compositing forward from a KernelTimer summary: algorithmic HBM
+    bytes / live CUDA-event launch time against MEASURED_PEAKS' HBM, plus
+    the issue roofline (warp instructions per launch from the committed ncu capture, scaled
+    by the live instance count) that actually bounds it."""
+    import torch
+
+    rec = None
+    for name in ("vegs_composite_forward", "vegs_composite_forward_fast"):
+        if name in ksum:
+            rec = ksum[name]
+            break
+    if rec is None:
+        return None
+    peak, peak_kind = peaks()
+    byts = [algorithmic_bytes("vegs_composite_forward", nk, ni, pixels) for nk, ni in rec["counts"]]
+    achieved = sum(byts) / len(byts) / (rec["avg_ms"] / 1000.0) / 1e9
+    out = {"bound": "hbm", "kernel": "vegs_composite_forward", "achieved": achieved, "peak": peak,
+           "peak_source": peak_kind, "unit": "GB/s", "frac": achieved / peak, "traffic": None,
+           "algorithmic_bytes_per_launch": sum(byts) / len(byts), "avg_launch_ms": rec["avg_ms"],
+           "launches": rec["launches"], "avg_instances": sum(c[1] for c in rec["counts"]) / len(rec["counts"])}
+    prof = ROOT / "profiles" / ncu_file
+    if prof.exists():
+        r = json.loads(prof.read_text()).get(ncu_key)
+        if r:
+            scale = out["avg_instances"] / r["instances"] if r.get("instances") else 1.0
+            out["traffic"] = r["dram_bytes"] * scale
+            mhz = MAX_SM_MHZ
+            try:
+                mhz = float(json.loads((ROOT / "MEASURED_PEAKS.json").read_text())["sm_max_mhz"])
+            except Exception:
+                pass
+            sms = torch.cuda.get_device_properties(torch.cuda.current_device()).multi_processor_count
+            peak_issue = sms * 4 * mhz * 1e6
+            wi = r["warp_instructions"] * scale
+            out["issue_roofline"] = {"bound": "issue", "achieved": wi / (rec["avg_ms"] / 1000.0), "peak": peak_issue,
+                                     "unit": "warp-instructions/s",
+                                     "frac": wi / (rec["avg_ms"] / 1000.0) / peak_issue,
+                                     "warp_instructions_per_launch": wi,
+                                     "source": f"profiles/{ncu_file}[{ncu_key}]"
+                                               + (" scaled by live/profiled instances" if scale != 1.0 else "")}
+    return out
 
 
 def algorithmic_bytes(name: str, n_kept: int, n_inst: int, pixels: int, n_ch: int = 3) -> float:
@@ -334,6 +380,15 @@ def run_b200(args) -> None:
     rms = max_over_ranks(r0.elapsed_time(r1))
     px = args.render_frames * VIEWS_PER_STEP * 1024 * 1024
     render_mpx_s = px / (rms / 1000.0) / 1e6
+    # kernel-timing pass of the render (events on each lane's stream), for its roofline
+    rtimer = KernelTimer(None)
+    for _, rz in pipe.lanes:
+        rz.timer = rtimer
+    pipe.render(trainer.params, trainer.n, items)
+    torch.cuda.synchronize()
+    for _, rz in pipe.lanes:
+        rz.timer = None
+    render_roof = composite_roofline(rtimer.summary(), 1024 * 1024, "vegs_composite_forward")
     del pipe
 
     # ---- end to end through the public API with host buffers: the views carry their
@@ -356,6 +411,15 @@ def run_b200(args) -> None:
     e2e_ms = max_over_ranks(max(s0.elapsed_time(s1), wall * 1000.0)) / args.steps
     e2e = {"value": 1000.0 / e2e_ms, "unit": UNIT, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": 8,
            "ms_per_step": e2e_ms}
+
+    # ---- the reference-shaped numpy API (the drop-in a vegsplat training loop calls,
+    # train.py:469-483): render_with_state -> compute_loss -> rasterize_backward per view,
+    # mean gradient, adam_step; every array crosses PCIe as numpy.  Timed on rank 0's
+    # first views (host wall clock with a device sync), extrapolated to the 16-view step.
+    api = None
+    if rank == 0 and not args.no_api:
+        api = run_api_path(learned, tf, [cams[i] for i in mine], [t.numpy() for t in host_targets], args.api_views)
+    torch.cuda.empty_cache()
 
     # the config-3 sweep and the config-4 run have their own barriers / max-over-ranks:
     # every rank takes part
@@ -417,15 +481,68 @@ def run_b200(args) -> None:
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": max(args.warmup, 3), "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f32+f64", "data": "synthetic (seeded, scenes.py)",
-            "config": config_block(world, args.backend), "e2e": e2e, "render_mpx_s": render_mpx_s, "loss": loss_val,
+            "config": config_block(world, args.backend), "e2e": e2e, "render_mpx_s": render_mpx_s,
+            "render_roofline": render_roof, "loss": loss_val,
             "gpu_launches": int(launches), "roofline": roof, "kernels": kernels, "stages": stages,
             "render_sweep_c3": sweep,
+            "api_path_c2": api,
             "train_densify_c4": c4,
             "cpu_baseline": cpu,
             "clocks": clk}
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def run_api_path(learned, tf, cams, targets, n_views: int) -> dict:
+    import torch
+
+    from paper_2504_13339_b200 import raster as R
+    from paper_2504_13339_b200.loss import compute_loss
+    from paper_2504_13339_b200.train import OptimizerState, TrainConfig, adam_step
+
+    cfg = TrainConfig(iterations=30000)
+
+    class LossCfg:
+        lambda_ssim = 0.2
+        normal_loss_weight = 0.0
+        smooth_loss_weight = 0.0
+
+    gs = learned.select(np.arange(len(learned)))  # a private copy: adam_step updates it in place
+    opt = OptimizerState.for_set(gs)
+
+    def one_view(i):
+        img, st = R.render_with_state(gs, tf, cams[i], (1.0, 1.0, 1.0), with_aux=False, dtype=np.float32)
+        _, ig, _ = compute_loss(img, targets[i], LossCfg())
+        return R.rasterize_backward(st, ig)
+
+    one_view(0)  # warm-up (allocations)
+    torch.cuda.synchronize()
+    n = min(n_views, len(cams))
+    view_s, acc = [], None
+    for i in range(n):
+        t0 = time.perf_counter()
+        g = one_view(i)
+        if acc is None:
+            acc = g
+        else:
+            for k, a in g.arrays().items():
+                getattr(acc, k)[...] += a
+        torch.cuda.synchronize()
+        view_s.append(time.perf_counter() - t0)
+    for k, a in acc.arrays().items():
+        a /= n
+    t0 = time.perf_counter()
+    adam_step(gs, acc, opt, cfg, 1)
+    torch.cuda.synchronize()
+    adam_s = time.perf_counter() - t0
+    step_s = VIEWS_PER_STEP * statistics.mean(view_s) + adam_s
+    return {"workload": "c2 through the numpy drop-in API (raster.render_with_state f32 + loss.compute_loss + "
+                        "raster.rasterize_backward per view, train.adam_step), host wall clock",
+            "steps_per_s": 1.0 / step_s, "ms_per_view": 1000.0 * statistics.mean(view_s),
+            "adam_ms": 1000.0 * adam_s, "views_timed": n,
+            "note": f"extrapolated x{VIEWS_PER_STEP}/{n}; params, gradients and Adam moments cross PCIe as float64 "
+                    "numpy every call (~0.6 GB per Adam step), which the device-resident Trainer avoids"}
 
 
 def run_sweep(args, dev, rank, world) -> dict:
@@ -466,10 +583,19 @@ def run_sweep(args, dev, rank, world) -> dict:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
     renders = 8 * n_frames
+    stimer = KernelTimer(None)
+    for _, rz in pipe.lanes:
+        rz.timer = stimer
+    pipe.render(params, len(gs), items)
+    torch.cuda.synchronize()
+    for _, rz in pipe.lanes:
+        rz.timer = None
+    roof = composite_roofline(stimer.summary(), 1920 * 1080, "vegs_composite_forward_c3")
     return {"workload": "c3: 3M blob-shaped Gaussians, 1920x1080, 8 random 256-knot TFs per frame (1-6 bumps), "
                         "forward render per (frame, TF), frames sharded across ranks",
             "renders": renders, "ms_per_render": ms / (renders / world), "mpx_s": renders * 1920 * 1080 / (ms / 1e3) / 1e6,
-            "tf_frames_per_s": renders / (ms / 1e3), "avg_instances": inst / max(len(mine) * 8, 1)}
+            "tf_frames_per_s": renders / (ms / 1e3), "avg_instances": inst / max(len(mine) * 8, 1),
+            "roofline": roof}
 
 
 def run_c4(args, dev, rank, world) -> dict:

@@ -6,6 +6,7 @@
 // unit (preprocess.cu) buys nothing here and costs ~a quarter of the FP64 instructions.
 
 #include <math.h>
+#include <stdlib.h>
 
 #include "preprocess_common.cuh"
 
@@ -82,6 +83,106 @@ __global__ void __launch_bounds__(VEGS_RR_T) reduce_rows_kernel(const uint32_t *
     }
 #pragma unroll
     for (int k = 0; k < NV; ++k) sums[(int64_t)NV * g + k] = acc[k];
+}
+
+// The same sums, warp-cooperative (the per-thread walks above keep ~3.6 of 32 lanes busy:
+// the visited-row counts of neighbouring Gaussians differ a lot).  A warp owns 32
+// consecutive Gaussians, i.e. one contiguous span of duplicate-order rows.  It scans the
+// span's visited words 32 at a time and compacts the visited rows into batches of 32
+// (SMEM); per batch every lane loads one row (contiguous rows: coalesced), finds its
+// Gaussian by a 5-step search over the warp's 32 offsets, and stages the row in SMEM; the
+// first lane of each Gaussian's run then adds the run's rows, in ascending row order, to
+// that Gaussian's float64 accumulator.  Every accumulator therefore sees exactly the
+// additions of reduce_rows_kernel in the same order: bitwise the same sums.
+#ifndef VEGS_RRW_WARPS
+#define VEGS_RRW_WARPS 4
+#endif
+template <typename Real, int NV>
+__global__ void __launch_bounds__(32 * VEGS_RRW_WARPS) reduce_rows_warp_kernel(const int64_t *offsets,
+                                                                               const Real *rows, int64_t n,
+                                                                               const uint32_t *visited,
+                                                                               double *sums) {
+    constexpr int RS = ((7 + (NV - 6)) + 3) & ~3;
+    constexpr int NF4 = (int)(RS * sizeof(Real) / 16);
+    __shared__ int64_t s_p[VEGS_RRW_WARPS][64];           // compacted visited rows (up to 63 pending)
+    __shared__ __align__(16) Real s_row[VEGS_RRW_WARPS][32][RS];
+    __shared__ int8_t s_own[VEGS_RRW_WARPS][33];
+    __shared__ double s_acc[VEGS_RRW_WARPS][32][NV + 1];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t g0 = ((int64_t)blockIdx.x * VEGS_RRW_WARPS + warp) * 32;
+    if (g0 >= n) return;
+    const int64_t off_l = __ldg(offsets + (g0 + lane < n ? g0 + lane : n));
+    const int64_t p_begin = __shfl_sync(0xffffffffu, off_l, 0);
+    const int64_t p_end = __ldg(offsets + (g0 + 32 < n ? g0 + 32 : n));
+#pragma unroll
+    for (int k = 0; k < NV; ++k) s_acc[warp][lane][k] = 0.0;
+    int64_t *bp = s_p[warp];
+    int fill = 0;
+    auto flush = [&](int m) {  // m visited rows in bp[0..m)
+        const int64_t p = lane < m ? bp[lane] : INT64_MAX;
+        int lo = 0;  // last local Gaussian whose offset is <= p (every lane in the shuffles)
+#pragma unroll
+        for (int step = 16; step >= 1; step >>= 1) {
+            const int cand = lo + step;
+            const int64_t oc = __shfl_sync(0xffffffffu, off_l, cand & 31);
+            if (cand < 32 && oc <= p) lo = cand;
+        }
+        if (lane < m) {
+            s_own[warp][lane] = (int8_t)lo;
+            const float4 *src = reinterpret_cast<const float4 *>(rows + (int64_t)RS * p);
+#pragma unroll
+            for (int k = 0; k < NF4; ++k) reinterpret_cast<float4 *>(s_row[warp][lane])[k] = __ldg(src + k);
+        } else if (lane == m) {
+            s_own[warp][lane] = -1;
+        }
+        __syncwarp();
+        if (lane < m) {
+            const int o = s_own[warp][lane];
+            if (lane == 0 || s_own[warp][lane - 1] != o) {  // head of o's run in this batch
+                double a[NV];
+#pragma unroll
+                for (int k = 0; k < NV; ++k) a[k] = s_acc[warp][o][k];
+                for (int r = lane; r < m && s_own[warp][r] == o; ++r) {
+#pragma unroll
+                    for (int k = 0; k < NV; ++k) a[k] = a[k] + (double)s_row[warp][r][k];
+                }
+#pragma unroll
+                for (int k = 0; k < NV; ++k) s_acc[warp][o][k] = a[k];
+            }
+        }
+        __syncwarp();
+    };
+    if (p_end > p_begin) {
+        const int64_t w_lo = p_begin >> 5, w_hi = (p_end - 1) >> 5;
+        for (int64_t wb = w_lo; wb <= w_hi; wb += 32) {
+            const int64_t wi = wb + lane;
+            uint32_t word = 0;
+            if (wi <= w_hi) {
+                word = __ldg(visited + wi);
+                if (wi == w_lo) word &= ~0u << (uint32_t)(p_begin & 31);
+                if (wi == w_hi && ((p_end & 31) != 0)) word &= (1u << (uint32_t)(p_end & 31)) - 1u;
+            }
+            const int nw = (int)(w_hi - wb + 1 < 32 ? w_hi - wb + 1 : 32);
+            for (int k = 0; k < nw; ++k) {
+                const uint32_t bits = __shfl_sync(0xffffffffu, word, k);
+                if (!bits) continue;
+                if ((bits >> lane) & 1u) bp[fill + __popc(bits & ((1u << lane) - 1u))] = ((wb + k) << 5) + lane;
+                fill += __popc(bits);
+                __syncwarp();
+                if (fill >= 32) {
+                    flush(32);
+                    if (lane < fill - 32) bp[lane] = bp[32 + lane];
+                    fill -= 32;
+                    __syncwarp();
+                }
+            }
+        }
+        if (fill > 0) flush(fill);
+    }
+    if (g0 + lane < n) {
+#pragma unroll
+        for (int k = 0; k < NV; ++k) sums[(int64_t)NV * (g0 + lane) + k] = s_acc[warp][lane][k];
+    }
 }
 
 // Backward, part 2: projection and shading adjoints per Gaussian (float64).
@@ -289,7 +390,17 @@ extern "C" int vegs_preprocess_backward(const double *params, int64_t n, const V
     const int rr_blocks = (int)((n + VEGS_RR_T - 1) / VEGS_RR_T);
     cudaStream_t s = (cudaStream_t)stream;
     double *sums = (double *)ws;
-    if (store_f64) {
+    const char *per_thread = getenv("VEGS_RR_PER_THREAD");  // test switch: the per-Gaussian walk
+    if (!(per_thread && per_thread[0] && per_thread[0] != '0')) {
+        const int wb = (int)((n + 32 * VEGS_RRW_WARPS - 1) / (32 * VEGS_RRW_WARPS));
+        if (store_f64) {
+            if (n_channels == 3) reduce_rows_warp_kernel<double, 9><<<wb, 32 * VEGS_RRW_WARPS, 0, s>>>(offsets, (const double *)inst_rows, n, inst_visited, sums);
+            else reduce_rows_warp_kernel<double, 17><<<wb, 32 * VEGS_RRW_WARPS, 0, s>>>(offsets, (const double *)inst_rows, n, inst_visited, sums);
+        } else {
+            if (n_channels == 3) reduce_rows_warp_kernel<float, 9><<<wb, 32 * VEGS_RRW_WARPS, 0, s>>>(offsets, (const float *)inst_rows, n, inst_visited, sums);
+            else reduce_rows_warp_kernel<float, 17><<<wb, 32 * VEGS_RRW_WARPS, 0, s>>>(offsets, (const float *)inst_rows, n, inst_visited, sums);
+        }
+    } else if (store_f64) {
         if (n_channels == 3) reduce_rows_kernel<double, 9><<<rr_blocks, VEGS_RR_T, 0, s>>>(tiles, offsets, (const double *)inst_rows, n, inst_visited, sums);
         else reduce_rows_kernel<double, 17><<<rr_blocks, VEGS_RR_T, 0, s>>>(tiles, offsets, (const double *)inst_rows, n, inst_visited, sums);
     } else {

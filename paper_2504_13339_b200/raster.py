@@ -15,7 +15,7 @@ parameters, no per-call host copies).
 
 from __future__ import annotations
 
-from dataclasses import dataclass, field
+from dataclasses import dataclass
 
 import numpy as np
 import torch
@@ -174,20 +174,101 @@ class BlendState:
         return self._get("ncon", lambda: _np(self._frame.n_contrib).reshape(self.height, self.width))
 
 
-@dataclass
+# -- lazy device views of the per-Gaussian caches (render_with_state's RenderState) ----------
+# The reference's ShadeResult / ProjectResult hold ~17 + 7 float64 arrays per Gaussian (270 MB
+# at 1M Gaussians); here each field is copied to numpy only when it is first read, so a
+# render -> loss -> backward iteration moves just the image and the gradients over PCIe.
+
+_AUX_COLS = {"v": 0, "w": 1, "opacity": 2, "cmap": (3, 6), "light": (6, 9), "light_dist": 9, "n_hat": (10, 13),
+             "n_norm": 13, "ndotl": 14, "ka": 15, "kd": 16, "ks": 17, "beta": 18, "spec_pow": 19, "cov2d": (20, 23)}
+_API_COLS = {"mean2d": 2, "conic": 3, "color": 3}
+
+
+class _FrameViews:
+    """numpy copies of a forward's per-Gaussian api tables, column by column, cached."""
+
+    def __init__(self, fr: Frame, n: int):
+        self.fr, self.n, self.cache = fr, n, {}
+
+    def get(self, name: str) -> np.ndarray:
+        if name in self.cache:
+            return self.cache[name]
+        fr, n = self.fr, self.n
+        if name in _AUX_COLS:
+            c = _AUX_COLS[name]
+            aux = fr.api["aux"][: 24 * n].view(n, 24)
+            out = _np(aux[:, c[0]:c[1]] if isinstance(c, tuple) else aux[:, c]).copy()
+        elif name == "visible":
+            out = _np(fr.api["visible"][:n]).astype(bool)
+        elif name == "kept":
+            out = _np(torch.nonzero(fr.tiles[:n] != 0).flatten()).astype(np.int64)
+        elif name == "rect":
+            out = _np(fr.rect[: 4 * n].view(n, 4)).astype(np.int32)
+        else:
+            k = _API_COLS.get(name, 1)
+            t = fr.api[name][: k * n]
+            out = _np(t.view(n, k) if k > 1 else t)
+        self.cache[name] = out
+        return out
+
+
+class LazyShadeResult:
+    """ShadeResult (shading.py:30-49) whose float64 fields are device-resident until read."""
+
+    FIELDS = ("color", "alpha_base", "visible", "v", "w", "opacity", "cmap", "light", "light_dist", "n_hat",
+              "n_norm", "ndotl", "ka", "kd", "ks", "beta", "spec_pow")
+
+    def __init__(self, views: _FrameViews):
+        self._views = views
+
+    def __getattr__(self, name):
+        if name in LazyShadeResult.FIELDS:
+            return self._views.get(name)
+        raise AttributeError(name)
+
+    def materialize(self) -> ShadeResult:
+        return ShadeResult(**{k: getattr(self, k) for k in self.FIELDS})
+
+
+class LazyProjectResult:
+    """ProjectResult (projection.py:43-66) on the kept subset, device-resident until read."""
+
+    FIELDS = ("in_view", "mean2d", "conic", "cov2d", "depth", "radius", "rect")
+
+    def __init__(self, views: _FrameViews):
+        self._views = views
+
+    def __getattr__(self, name):
+        v = self._views
+        if name == "in_view":
+            key = "_in_view"
+            if key not in v.cache:
+                v.cache[key] = np.isin(np.flatnonzero(v.get("visible")), v.get("kept"))
+            return v.cache[key]
+        if name in LazyProjectResult.FIELDS:
+            key = "_p_" + name
+            if key not in v.cache:
+                v.cache[key] = np.ascontiguousarray(v.get(name)[v.get("kept")])
+            return v.cache[key]
+        raise AttributeError(name)
+
+    def materialize(self) -> ProjectResult:
+        return ProjectResult(**{k: getattr(self, k) for k in self.FIELDS})
+
+
 class RenderState:
-    gs: GaussianSet
-    tf: TransferFunction
-    camera: Camera
-    settings: RasterSettings
-    shade_cache: ShadeResult
-    proj: ProjectResult
-    kept: np.ndarray
-    blend: BlendState
-    with_aux: bool
-    image: ImageBuffer
-    _frame: Frame = field(default=None, repr=False)
-    _rz: Rasterizer = field(default=None, repr=False)
+    """pipeline.py:77-90: references to gs / tf / camera plus the forward's caches.
+    ``shade_cache``, ``proj`` and ``kept`` are lazy device views (see LazyShadeResult)."""
+
+    def __init__(self, gs, tf, camera, settings, shade_cache, proj, kept, blend, with_aux, image, _frame=None,
+                 _rz=None):
+        self.gs, self.tf, self.camera, self.settings = gs, tf, camera, settings
+        self.shade_cache, self.proj, self._kept = shade_cache, proj, kept
+        self.blend, self.with_aux, self.image, self._frame, self._rz = blend, with_aux, image, _frame, _rz
+
+    @property
+    def kept(self) -> np.ndarray:
+        return self._kept.get("kept") if isinstance(self._kept, _FrameViews) else self._kept
 
 
 @dataclass
@@ -319,11 +400,12 @@ def render_with_state(gs: GaussianSet, tf: TransferFunction, camera: Camera,
     rz = Rasterizer(settings, n_ch, _dtype_flag(dtype), pooled=False)
     params = _upload_params(gs, dev)
     fr = rz.forward(params, len(gs), DeviceTF(tf, dev), camera, background, want_order=True, api_views=True)
-    data, sh, proj, kept = _splat_views(fr, len(gs), with_aux)
+    views = _FrameViews(fr, len(gs))
     img = _image_from_frame(fr, n_ch)
-    blend = BlendState(fr, dtype, settings, len(kept))
-    state = RenderState(gs=gs, tf=tf, camera=camera, settings=settings, shade_cache=sh, proj=proj, kept=kept,
-                        blend=blend, with_aux=with_aux, image=img, _frame=fr, _rz=rz)
+    blend = BlendState(fr, dtype, settings, fr.n_kept)
+    state = RenderState(gs=gs, tf=tf, camera=camera, settings=settings, shade_cache=LazyShadeResult(views),
+                        proj=LazyProjectResult(views), kept=views, blend=blend, with_aux=with_aux, image=img,
+                        _frame=fr, _rz=rz)
     return img, state
 
 

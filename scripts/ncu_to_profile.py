@@ -12,7 +12,10 @@ NCU = "/usr/local/cuda/bin/ncu"
 NAMES = {"composite_fwd2_kernel": "vegs_composite_forward", "composite_bwd4_kernel": "vegs_composite_backward"}
 
 
-def main(rep, out="profiles/ncu_composite.json"):
+def main(rep, out="profiles/ncu_composite.json", suffix="", instances=None, merge=False):
+    """suffix: appended to the keys (e.g. "_c3" for the config-3 render capture);
+    instances: the capture's tile-instance count (bench scales per-launch figures by it);
+    merge: update an existing json instead of replacing it."""
     raw = subprocess.run([NCU, "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(raw)))
     hdr = rows[0]
@@ -26,7 +29,7 @@ def main(rep, out="profiles/ncu_composite.json"):
         key = next((v for k, v in NAMES.items() if k in kname), None)
         if key is None:
             continue
-        res[key] = {
+        res[key + suffix] = {
             "dram_bytes": val(r, "dram__bytes_read.sum") * 1e6 + val(r, "dram__bytes_write.sum") * 1e6
             if "Mbyte" in rows[1][hdr.index("dram__bytes_read.sum")] else
             val(r, "dram__bytes_read.sum") + val(r, "dram__bytes_write.sum"),
@@ -35,10 +38,28 @@ def main(rep, out="profiles/ncu_composite.json"):
             "ncu_duration_us": val(r, "gpu__time_duration.sum") * (1e3 if rows[1][hdr.index("gpu__time_duration.sum")] == "ms" else 1.0),
             "registers": val(r, "launch__registers_per_thread"),
         }
-    res["_source"] = f"ncu --set full --clock-control none, one config-2 view ({Path(rep).name}); per launch"
+        if instances:
+            res[key + suffix]["instances"] = float(instances)
+    src = f"ncu --set full --clock-control none ({Path(rep).name}); per launch"
+    if merge and Path(out).exists():
+        old = json.loads(Path(out).read_text())
+        old.update({k: v for k, v in res.items()})
+        old["_source" + suffix] = src
+        res = old
+    else:
+        res["_source" + suffix] = src
     Path(out).write_text(json.dumps(res, indent=1) + "\n")
     print(json.dumps(res, indent=1))
 
 
 if __name__ == "__main__":
-    main(*sys.argv[1:])
+    import argparse
+
+    ap = argparse.ArgumentParser()
+    ap.add_argument("rep")
+    ap.add_argument("--out", default="profiles/ncu_composite.json")
+    ap.add_argument("--suffix", default="")
+    ap.add_argument("--instances", type=float, default=None)
+    ap.add_argument("--merge", action="store_true")
+    a = ap.parse_args()
+    main(a.rep, a.out, a.suffix, a.instances, a.merge)

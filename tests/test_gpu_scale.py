@@ -429,3 +429,22 @@ def test_densify_config4_rule_matches_oracle(cap):
         ref = op[k]
         assert np.abs(getattr(gp, k) - ref).max() <= 1e-12 * max(np.abs(ref).max(), 1.0), k
         assert np.array_equal(getattr(gm, k), om[k]) and np.array_equal(getattr(gv, k), ov[k]), k
+
+
+@pytest.mark.parametrize("n_ch", [3, 11])
+def test_warp_row_reduction_bitwise_equals_per_thread_walk(monkeypatch, n_ch):
+    """The warp-cooperative per-Gaussian row reduction adds every visited row in the same
+    ascending order as the per-thread walk (VEGS_RR_PER_THREAD=1): bitwise equal gradients."""
+    gs = scenes.blob_gaussians(150_000, seed=1)
+    params = torch.from_numpy(gs.pack()).cuda()
+    cam = scenes.orbit_cameras(1, 4, 640, 480)[0]
+    tf = DeviceTF(scenes.random_tf(1001))
+    rz = Rasterizer(n_channels=n_ch)
+    fr = rz.forward(params, len(gs), tf, cam)
+    d_img = torch.rand(480, 640, n_ch, device="cuda", generator=torch.Generator("cuda").manual_seed(2)) - 0.5
+    out = []
+    for per_thread in ("0", "1"):
+        monkeypatch.setenv("VEGS_RR_PER_THREAD", per_thread)
+        out.append(rz.backward(fr, d_img).clone())
+    assert torch.equal(out[0], out[1])
+    assert out[0].abs().max() > 0
