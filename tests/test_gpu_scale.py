@@ -432,9 +432,10 @@ def test_densify_config4_rule_matches_oracle(cap):
 
 
 @pytest.mark.parametrize("n_ch", [3, 11])
-def test_warp_row_reduction_bitwise_equals_per_thread_walk(monkeypatch, n_ch):
-    """The warp-cooperative per-Gaussian row reduction adds every visited row in the same
-    ascending order as the per-thread walk (VEGS_RR_PER_THREAD=1): bitwise equal gradients."""
+def test_float32_backward_chain_close_to_float64_chain(monkeypatch, n_ch):
+    """The float32-blend backward's adjoint chain runs in float32 (decisions in float64);
+    against the float64 chain (VEGS_BWD_CHAIN_F64=1) every class agrees far inside the
+    1e-4 gradient bar, and the visibility / view-space norms feeding densification match."""
     gs = scenes.blob_gaussians(150_000, seed=1)
     params = torch.from_numpy(gs.pack()).cuda()
     cam = scenes.orbit_cameras(1, 4, 640, 480)[0]
@@ -443,8 +444,16 @@ def test_warp_row_reduction_bitwise_equals_per_thread_walk(monkeypatch, n_ch):
     fr = rz.forward(params, len(gs), tf, cam)
     d_img = torch.rand(480, 640, n_ch, device="cuda", generator=torch.Generator("cuda").manual_seed(2)) - 0.5
     out = []
-    for per_thread in ("0", "1"):
-        monkeypatch.setenv("VEGS_RR_PER_THREAD", per_thread)
-        out.append(rz.backward(fr, d_img).clone())
-    assert torch.equal(out[0], out[1])
-    assert out[0].abs().max() > 0
+    for chain64 in ("0", "1"):
+        monkeypatch.setenv("VEGS_BWD_CHAIN_F64", chain64)
+        vs = torch.empty(len(gs), dtype=torch.float64, device="cuda")
+        vis = torch.empty(len(gs), dtype=torch.uint8, device="cuda")
+        g = rz.backward(fr, d_img, viewspace_norm=vs, visible=vis).clone()
+        out.append((g.cpu().numpy(), vs.cpu().numpy(), vis.cpu().numpy()))
+    from paper_2504_13339_b200.model import GaussianSet
+
+    a, b = GaussianSet.unpack(out[0][0], len(gs)), GaussianSet.unpack(out[1][0], len(gs))
+    for k in PARAM_CLASSES:
+        assert G.norm_rel(getattr(a, k), getattr(b, k)) <= 1e-5, (k, G.norm_rel(getattr(a, k), getattr(b, k)))
+    assert np.array_equal(out[0][2], out[1][2])
+    assert G.norm_rel(out[0][1], out[1][1]) <= 1e-6
