@@ -457,3 +457,31 @@ def test_float32_backward_chain_close_to_float64_chain(monkeypatch, n_ch):
         assert G.norm_rel(getattr(a, k), getattr(b, k)) <= 1e-5, (k, G.norm_rel(getattr(a, k), getattr(b, k)))
     assert np.array_equal(out[0][2], out[1][2])
     assert G.norm_rel(out[0][1], out[1][1]) <= 1e-6
+
+
+@pytest.mark.parametrize("pair", ["0", "1"])
+@pytest.mark.parametrize("name", ["c0_f32", "dense_f32"])
+def test_paired_forward_bitwise_equals_single_entry_forward(monkeypatch, name, pair):
+    """The forward's loop with two list entries per iteration (default) and with one
+    (VEGS_FWD_PAIR=0) against the reference fixture: T, last contributor and contributor
+    count bit for bit."""
+    monkeypatch.setenv("VEGS_FWD_PAIR", pair)
+    d = G.load(name)
+    params = torch.from_numpy(G.gs_of(d).pack()).cuda()
+    cam = G.cam_of(d["cam"])
+    fr = Rasterizer(pooled=False).forward(params, len(d["gs_position"]), DeviceTF(G.tf_of(d)), cam, tuple(d["bg"]))
+    h, w = cam.height, cam.width
+    assert np.array_equal(fr.out_last.cpu().numpy().reshape(h, w), d["out_last"])
+    assert np.array_equal(fr.n_contrib.cpu().numpy().reshape(h, w), d["n_contrib"])
+    assert np.array_equal(fr.out_t.cpu().numpy().reshape(h, w), d["out_t"])
+
+
+@pytest.mark.slow
+def test_c2_single_entry_forward_vs_reference(monkeypatch, c2_ref):
+    monkeypatch.setenv("VEGS_FWD_PAIR", "0")
+    d, gs, cam, img, st = c2_ref
+    params = torch.from_numpy(gs.pack()).cuda()
+    fr = Rasterizer(pooled=False).forward(params, len(gs), DeviceTF(scenes.config_scene("c2")[2]), cam)
+    assert np.array_equal(digest(fr.out_last.cpu().numpy().astype(np.int64), np.int64), d["out_last_sha"])
+    assert np.array_equal(digest(fr.n_contrib.cpu().numpy(), np.int32), d["n_contrib_sha"])
+    assert np.array_equal(digest(fr.out_t.cpu().numpy(), np.float32), d["out_t_sha"])
