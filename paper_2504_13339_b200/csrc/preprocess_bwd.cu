@@ -20,7 +20,7 @@
 namespace vegs {
 
 // ---------------------------------------------------------------------------------
-// Backward, part 1: float64 sum of each kept Gaussian's instance rows, in duplicate order
+// Backward, part 1: the sum of each kept Gaussian's instance rows, in duplicate order
 // (== sorted-instance order per splat, the order np.add.at applies at pipeline.py:313-316).
 // A lean kernel (few registers, full occupancy, 16-byte loads); the visited bitmask
 // (L2-resident, one bit per instance) means only the ~30% of rows a pixel actually
@@ -39,9 +39,13 @@ __global__ void __launch_bounds__(VEGS_RR_T) reduce_rows_kernel(const uint32_t *
     if (cnt == 0) return;
     constexpr int RS = ((7 + (NV - 6)) + 3) & ~3;
     constexpr int NF4 = (int)(RS * sizeof(Real) / 16);
-    double acc[NV];
+    // float32 rows (float32 blends) are summed in float32 and widened once per Gaussian: a
+    // Gaussian has ~3 visited rows (<= ~50), so the sum is within ~1e-6 of the float64 one,
+    // and the per-row float -> double conversions (XU pipe, 71% busy) are gone
+    using Acc = Real;
+    Acc acc[NV];
 #pragma unroll
-    for (int k = 0; k < NV; ++k) acc[k] = 0.0;
+    for (int k = 0; k < NV; ++k) acc[k] = (Acc)0;
     // ascending duplicate-order index; only rows whose visited bit is set were written
     const int64_t p0 = offsets[g], pend = p0 + cnt;
     for (int64_t p = p0; p < pend;) {
@@ -76,13 +80,13 @@ __global__ void __launch_bounds__(VEGS_RR_T) reduce_rows_kernel(const uint32_t *
             for (int q = 0; q < Q; ++q)
                 if (b[q] >= 0) {
 #pragma unroll
-                    for (int k = 0; k < NV; ++k) acc[k] = acc[k] + (double)row[q][k];
+                    for (int k = 0; k < NV; ++k) acc[k] = acc[k] + row[q][k];
                 }
         }
         p += span;
     }
 #pragma unroll
-    for (int k = 0; k < NV; ++k) sums[(int64_t)NV * g + k] = acc[k];
+    for (int k = 0; k < NV; ++k) sums[(int64_t)NV * g + k] = (double)acc[k];
 }
 
 // Backward, part 2: projection and shading adjoints per Gaussian (float64).

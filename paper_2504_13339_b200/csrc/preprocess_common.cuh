@@ -114,10 +114,45 @@ struct Projected {
     int x0, x1, y0, y1;
 };
 
-__device__ void shade_one(const ParamView &P, int64_t g, const TFTable &tf, const VegsCamera &cam,
+// One Gaussian's 19 parameters loaded up front (read-only path, all loads in flight
+// together) behind ParamView's indexing: P.pos[3 * g + k] etc. read registers.  Kernels
+// that store (record, table) between parameter reads otherwise serialise the loads behind
+// the stores (the compiler must assume they may alias).
+template <int N>
+struct RegArr {
+    double v[N];
+};
+struct ParamRegs {
+    RegArr<3> pos, log_scale, normal;
+    RegArr<4> rot;
+    RegArr<1> raw_value, raw_weight, raw_ka, raw_kd, raw_ks, raw_beta;
+    __device__ __forceinline__ ParamRegs(const ParamView &P, int64_t g) {
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            pos.v[k] = __ldg(P.pos + 3 * g + k);
+            log_scale.v[k] = __ldg(P.log_scale + 3 * g + k);
+            normal.v[k] = __ldg(P.normal + 3 * g + k);
+        }
+#pragma unroll
+        for (int k = 0; k < 4; ++k) rot.v[k] = __ldg(P.rot + 4 * g + k);
+        raw_value.v[0] = __ldg(P.raw_value + g);
+        raw_weight.v[0] = __ldg(P.raw_weight + g);
+        raw_ka.v[0] = __ldg(P.raw_ka + g);
+        raw_kd.v[0] = __ldg(P.raw_kd + g);
+        raw_ks.v[0] = __ldg(P.raw_ks + g);
+        raw_beta.v[0] = __ldg(P.raw_beta + g);
+    }
+};
+// component k of Gaussian g's parameter (w values per Gaussian), from memory or registers
+__device__ __forceinline__ double pget(const double *a, int64_t g, int w, int k) { return a[w * g + k]; }
+template <int N>
+__device__ __forceinline__ double pget(const RegArr<N> &a, int64_t, int, int k) { return a.v[k]; }
+
+template <class PV>
+__device__ void shade_one(const PV &P, int64_t g, const TFTable &tf, const VegsCamera &cam,
                           const VegsSettings &st, Shaded &s) {
-    s.v = sigmoid(P.raw_value[g]);
-    s.w = sigmoid(P.raw_weight[g]);
+    s.v = sigmoid(pget(P.raw_value, g, 1, 0));
+    s.w = sigmoid(pget(P.raw_weight, g, 1, 0));
     const double vc = clip01(s.v);
     // np.interp on both maps (the three colour channels share one segment search)
     if (vc != vc) {
@@ -139,24 +174,24 @@ __device__ void shade_one(const ParamView &P, int64_t g, const TFTable &tf, cons
     s.alpha_base = s.op * s.w;
     double d[3], nn2 = 0.0, dd2 = 0.0;
     for (int k = 0; k < 3; ++k) {
-        d[k] = cam.position[k] - P.pos[3 * g + k];
+        d[k] = cam.position[k] - pget(P.pos, g, 3, k);
         dd2 = dd2 + d[k] * d[k];
     }
     s.dist = sqrt(dd2);
     for (int k = 0; k < 3; ++k) s.light[k] = d[k] / s.dist;
-    for (int k = 0; k < 3; ++k) nn2 = nn2 + P.normal[3 * g + k] * P.normal[3 * g + k];
+    for (int k = 0; k < 3; ++k) nn2 = nn2 + pget(P.normal, g, 3, k) * pget(P.normal, g, 3, k);
     s.n_norm = sqrt(nn2);
     const double nd = fmax(s.n_norm, 1e-30);
     s.ndotl = 0.0;
     for (int k = 0; k < 3; ++k) {
-        s.n_hat[k] = P.normal[3 * g + k] / nd;
+        s.n_hat[k] = pget(P.normal, g, 3, k) / nd;
         s.ndotl = s.ndotl + s.n_hat[k] * s.light[k];
     }
     const double sa = fabs(s.ndotl);
-    s.ka = sigmoid(P.raw_ka[g]);
-    s.kd = sigmoid(P.raw_kd[g]);
-    s.ks = sigmoid(P.raw_ks[g]);
-    s.beta = fmin(fmax(exp(P.raw_beta[g]), kBetaMin), kBetaMax);
+    s.ka = sigmoid(pget(P.raw_ka, g, 1, 0));
+    s.kd = sigmoid(pget(P.raw_kd, g, 1, 0));
+    s.ks = sigmoid(pget(P.raw_ks, g, 1, 0));
+    s.beta = fmin(fmax(exp(pget(P.raw_beta, g, 1, 0)), kBetaMin), kBetaMax);
     s.spec = sa > 0.0 ? pow(fmax(sa, 1e-300), s.beta) : 0.0;
     const double diffuse = s.ka + s.kd * sa;
     const double specular = s.ks * s.spec;
@@ -164,12 +199,12 @@ __device__ void shade_one(const ParamView &P, int64_t g, const TFTable &tf, cons
     s.visible = s.alpha_base >= st.cull_alpha;
 }
 
-template <bool kRect = true>
-__device__ void project_one(const ParamView &P, int64_t g, double alpha_base, const VegsCamera &cam,
+template <bool kRect = true, class PV>
+__device__ void project_one(const PV &P, int64_t g, double alpha_base, const VegsCamera &cam,
                             const VegsSettings &st, Projected &p) {
     const double *W = cam.rot;
     double d[3];
-    for (int k = 0; k < 3; ++k) d[k] = P.pos[3 * g + k] - cam.position[k];
+    for (int k = 0; k < 3; ++k) d[k] = pget(P.pos, g, 3, k) - cam.position[k];
     for (int i = 0; i < 3; ++i) p.t[i] = d[0] * W[3 * i] + d[1] * W[3 * i + 1] + d[2] * W[3 * i + 2];
     const double tz = p.t[2];
     const bool front = tz > cam.near_z;
@@ -187,7 +222,7 @@ __device__ void project_one(const ParamView &P, int64_t g, double alpha_base, co
 
     double q[4], qq = 0.0;
     for (int k = 0; k < 4; ++k) {
-        q[k] = P.rot[4 * g + k];
+        q[k] = pget(P.rot, g, 4, k);
         qq = qq + q[k] * q[k];
     }
     p.q_norm = sqrt(qq);
@@ -205,7 +240,7 @@ __device__ void project_one(const ParamView &P, int64_t g, double alpha_base, co
     p.R[2][2] = 1 - 2 * (x * x + y * y);
     double s2[3];
     for (int k = 0; k < 3; ++k) {
-        p.scale[k] = exp(P.log_scale[3 * g + k]);
+        p.scale[k] = exp(pget(P.log_scale, g, 3, k));
         s2[k] = p.scale[k] * p.scale[k];
     }
     for (int i = 0; i < 3; ++i)
