@@ -14,6 +14,7 @@
  *                               + raster/pipeline.py:137-160 build_splat_data, pipeline.py:207-215 (pmin,
  *                               f32 instance cast)
  *   vegs_bin_count / vegs_bin_sort
+ *   vegs_bin_count_dev / _sort_dev  the same with the counts kept on the device (graph capture)
  *                               raster/pipeline.py:163-194 _build_instances (repeat + lexsort + searchsorted)
  *   vegs_composite_forward      raster/pipeline.py:197-237 rasterize_forward (tile blend on the splat table)
  *   vegs_composite_forward_fast the same with T carried in float32 (exact decisions; training / render path)
@@ -148,6 +149,23 @@ int vegs_bin_sort(const uint32_t *tiles, const uint64_t *depth_key, const int32_
                   uint32_t *sorted_gauss, uint32_t *inst_pid, int64_t *order,
                   int32_t *tile_start, int32_t *tile_end, int32_t *tile_order, void *ws,
                   size_t *ws_bytes, void *stream);
+
+/* Device-count binning (no host round trip per view; CUDA-graph capturable).
+ * vegs_bin_count_dev = vegs_bin_count, then: step_state[1] = max(step_state[1], n_instances);
+ * if n_instances > inst_capacity the view is emptied (counts, tiles, offsets zeroed: every
+ * later stage of the view runs on nothing, inside its buffers), *poison = 1 and
+ * step_state[0] = 1 (the caller grows its buffers and redoes the step; the trainer's Adam
+ * skips on it).  tiles is therefore read-write.  Same ws as vegs_bin_count.
+ * vegs_bin_sort_dev = vegs_bin_sort's counting placement with n_kept read from counts
+ * (device); launches and the workspace are sized for n kept splats.  Views above 12288
+ * tiles need the radix path and host counts: VEGS_ERR_ARG. */
+int vegs_bin_count_dev(uint32_t *tiles, int64_t n, int64_t *offsets, int64_t *kept_idx, int64_t *counts,
+                       int64_t inst_capacity, int64_t *step_state, int32_t *poison, void *ws,
+                       size_t *ws_bytes, void *stream);
+int vegs_bin_sort_dev(const uint64_t *depth_key, const int32_t *rect, const int64_t *offsets,
+                      const int64_t *kept_idx, int64_t n, const int64_t *counts, int32_t width,
+                      int32_t height, int32_t tile_size, uint32_t *sorted_gauss, int32_t *tile_start,
+                      int32_t *tile_end, int32_t *tile_order, void *ws, size_t *ws_bytes, void *stream);
 
 /* ---- composite -------------------------------------------------------------------- */
 /* Tile blend on the splat table.  out_img H x W x C, out_t H x W (storage type),
@@ -285,12 +303,15 @@ int vegs_adam_step(double *params, const double *grads, double *m, double *v, in
 
 /* The trainer's step update: g = ((grads0 + grads1) + grads2) + grads3 over the non-NULL
  * partial buffers (one per stream lane), written back into grads0, then Adam as
- * vegs_adam_step on g.  params == NULL: only the sum is formed (before a cross-rank
- * all-reduce; m, v, lr, nonfinite may then be NULL).  Replaces the trainer's eager
- * per-lane adds in front of train.py:176-195. */
+ * vegs_adam_step on g.  hyper (device, 12 float64): lr[10] per class, then the bias
+ * corrections 1 - beta1^t, 1 - beta2^t -- read at execution time, so a captured CUDA graph
+ * replays every step.  skip (device, nullable): when skip[0] != 0 nothing is updated (a
+ * view of the step overflowed its buffers, see vegs_bin_count_dev).  params == NULL: only
+ * the sum is formed (before a cross-rank all-reduce; m, v, hyper, nonfinite may be NULL).
+ * Replaces the trainer's eager per-lane adds in front of train.py:176-195. */
 int vegs_adam_step_sum(double *params, double *grads0, const double *grads1, const double *grads2,
-                       const double *grads3, double *m, double *v, int64_t n, const double *lr,
-                       double grad_scale, double bias1, double bias2, int32_t *nonfinite, void *stream);
+                       const double *grads3, double *m, double *v, int64_t n, const double *hyper,
+                       double grad_scale, int32_t *nonfinite, const int64_t *skip, void *stream);
 
 /* Library build identity (for the loader's sanity check). */
 const char *vegs_version(void);

@@ -71,7 +71,9 @@ __global__ void depth_key32_kernel(const uint64_t *key64, int64_t n, uint32_t *k
 // Runs of equal coarse keys among the kept splats are re-ordered by the exact float64 key
 // (insertion sort, strict comparison: the stable sort's index order survives among equal
 // float64 depths).  Runs are almost always of length 1-2.
-__global__ void depth_ties_kernel(const uint32_t *key32, const uint64_t *key64, int64_t n_kept, uint32_t *ids) {
+__global__ void depth_ties_kernel(const uint32_t *key32, const uint64_t *key64, int64_t n_kept, uint32_t *ids,
+                                  const int64_t *n_kept_dev = nullptr) {
+    if (n_kept_dev) n_kept = *n_kept_dev;  // device-count binning: grid sized for n
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i + 1 >= n_kept) return;
     const uint32_t k = key32[i];
@@ -192,7 +194,8 @@ __global__ void tile_weight_kernel(const int32_t *tile_start, const int32_t *til
 // rank) = depth rank order: exactly np.lexsort((depth, tile)), as the radix path.
 
 __global__ void chunk_count_kernel(const uint32_t *ids, const int4 *rect, int64_t n_kept, int C, int tiles_x,
-                                   int tiles_y, uint32_t *counts) {
+                                   int tiles_y, uint32_t *counts, const int64_t *n_kept_dev = nullptr) {
+    if (n_kept_dev) n_kept = *n_kept_dev;  // device-count binning: chunks past the kept splats count zero
     extern __shared__ int diff[];  // (tiles_y + 1) x (tiles_x + 1)
     const int c = blockIdx.x, W1 = tiles_x + 1, n_diff = (tiles_y + 1) * W1, n_tiles = tiles_x * tiles_y;
     for (int i = threadIdx.x; i < n_diff; i += blockDim.x) diff[i] = 0;
@@ -276,7 +279,8 @@ __global__ void chunk_offsets_kernel(uint32_t *counts, const uint32_t *gbase, co
 template <int kBands>
 __global__ void __launch_bounds__(32 * kBands) place_kernel(const uint32_t *ids, const int4 *rect, int64_t n_kept,
                                                             int C, int tiles_x, int tiles_y, const uint32_t *first,
-                                                            uint32_t *sorted_gauss) {
+                                                            uint32_t *sorted_gauss, const int64_t *n_kept_dev = nullptr) {
+    if (n_kept_dev) n_kept = *n_kept_dev;
     extern __shared__ uint32_t cursor[];
     const int n_tiles = tiles_x * tiles_y;
     const int c = blockIdx.x, lane = threadIdx.x & 31, band = threadIdx.x >> 5;
@@ -348,6 +352,33 @@ __global__ void placed_extras_kernel(const uint32_t *sorted_gauss, const int4 *r
         inst_pid[s] = (uint32_t)dup_index(__ldg(offsets + gid), __ldg(rect + gid), tx, ty);
     }
     if (order) order[s] = kept_idx[gid];
+}
+
+// Device-count binning (graph capture: no host round trip for the counts).  A view whose
+// instance count exceeds the caller's capacity is turned into an empty view: its counts,
+// tile counts and offsets are zeroed, so every later stage of the view (sort, compositing,
+// backward) runs on nothing and stays inside its buffers; step_state records the overflow
+// ([0] = 1) and the largest count seen ([1]) for the caller to grow its buffers and redo.
+__global__ void capacity_check_kernel(int64_t *counts, int64_t capacity, int64_t *step_state, int32_t *poison) {
+    const int64_t n_inst = counts[1];
+    atomicMax(reinterpret_cast<unsigned long long *>(step_state + 1), (unsigned long long)n_inst);
+    const bool over = n_inst > capacity;
+    *poison = over ? 1 : 0;
+    if (over) {
+        atomicExch(reinterpret_cast<unsigned long long *>(step_state), 1ull);
+        counts[0] = 0;
+        counts[1] = 0;
+    }
+}
+
+__global__ void capacity_empty_kernel(const int32_t *poison, uint32_t *tiles, int64_t n, int64_t *offsets,
+                                      int64_t *kept_idx) {
+    if (!*poison) return;
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i > n) return;
+    if (i < n) tiles[i] = 0u;
+    offsets[i] = 0;
+    kept_idx[i] = 0;
 }
 
 static size_t align_up(size_t x) { return (x + 255) & ~size_t(255); }
@@ -497,7 +528,14 @@ static int bin_place_impl(const uint64_t *depth_key, const int32_t *rect, const 
                           const int64_t *kept_idx, int64_t n, int64_t n_kept, int64_t n_inst, int tiles_x,
                           int tiles_y, uint32_t *sorted_gauss, uint32_t *inst_pid, int64_t *order,
                           int32_t *tile_start, int32_t *tile_end, int32_t *tile_order, void *ws, size_t *ws_bytes,
-                          cudaStream_t s) {
+                          cudaStream_t s, const int64_t *counts_dev = nullptr) {
+    // counts_dev (device-count binning): n_kept / n_inst live on the device; every launch is
+    // sized for n kept splats and the kernels read the real count (no host sync)
+    const int64_t *n_kept_dev = counts_dev;
+    if (counts_dev) {
+        n_kept = n;
+        n_inst = 1;  // unknown on the host; only its zero test below matters
+    }
     const int n_tiles = tiles_x * tiles_y;
 #ifndef VEGS_PLACE_CHUNKS
 #define VEGS_PLACE_CHUNKS 2048
@@ -553,13 +591,14 @@ static int bin_place_impl(const uint64_t *depth_key, const int32_t *rect, const 
         cub::DoubleBuffer<uint32_t> dk(dk0, dk1), dv(id0, id1);
         size_t tb = tb0;
         VEGS_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tb, dk, dv, (int64_t)n, 0, 32, s));
-        depth_ties_kernel<<<(int)((n_kept + 255) / 256), 256, 0, s>>>(dk.Current(), depth_key, n_kept, dv.Current());
+        depth_ties_kernel<<<(int)((n_kept + 255) / 256), 256, 0, s>>>(dk.Current(), depth_key, n_kept, dv.Current(),
+                                                                     n_kept_dev);
         VEGS_CHECK_LAUNCH();
         const uint32_t *ids = dv.Current();
         // 2. per-chunk tile counts -> first slot of every chunk in every tile, tile ranges
         const size_t diff_bytes = sizeof(int) * (size_t)(tiles_x + 1) * (tiles_y + 1);
         chunk_count_kernel<<<n_chunks, 256, diff_bytes, s>>>(ids, (const int4 *)rect, n_kept, C, tiles_x, tiles_y,
-                                                             counts);
+                                                             counts, n_kept_dev);
         VEGS_CHECK_LAUNCH();
         const int64_t ng = (int64_t)n_groups * n_tiles;
         chunk_group_sum_kernel<<<(int)((ng + 255) / 256), 256, 0, s>>>(counts, n_chunks, n_tiles, G, gsum);
@@ -574,12 +613,14 @@ static int bin_place_impl(const uint64_t *depth_key, const int32_t *rect, const 
         // 3. placement, one warp per chunk
         if (n_tiles <= 4096)
             place_kernel<8><<<n_chunks, 32 * 8, sizeof(uint32_t) * n_tiles, s>>>(ids, (const int4 *)rect, n_kept, C,
-                                                                               tiles_x, tiles_y, counts, sorted_gauss);
+                                                                               tiles_x, tiles_y, counts, sorted_gauss,
+                                                                               n_kept_dev);
         else
             place_kernel<4><<<n_chunks, 32 * 4, sizeof(uint32_t) * n_tiles, s>>>(ids, (const int4 *)rect, n_kept, C,
-                                                                               tiles_x, tiles_y, counts, sorted_gauss);
+                                                                               tiles_x, tiles_y, counts, sorted_gauss,
+                                                                               n_kept_dev);
         VEGS_CHECK_LAUNCH();
-        if (inst_pid || order) {
+        if ((inst_pid || order) && !counts_dev) {
             placed_extras_kernel<<<(int)((n_inst + 255) / 256), 256, 0, s>>>(
                 sorted_gauss, (const int4 *)rect, offsets, kept_idx, tile_end, n_inst, n_tiles, tiles_x, inst_pid,
                 order);
@@ -621,4 +662,33 @@ extern "C" int vegs_bin_sort(const uint32_t *tiles, const uint64_t *depth_key, c
                                        ws_bytes, s);
     return bin_sort_impl<uint32_t>(tiles, depth_key, rect, offsets, kept_idx, n, n_kept, n_inst, tiles_x, n_tiles,
                                    sorted_gauss, inst_pid, order, tile_start, tile_end, tile_order, ws, ws_bytes, s);
+}
+
+extern "C" int vegs_bin_count_dev(uint32_t *tiles, int64_t n, int64_t *offsets, int64_t *kept_idx, int64_t *counts,
+                                  int64_t inst_capacity, int64_t *step_state, int32_t *poison, void *ws,
+                                  size_t *ws_bytes, void *stream) {
+    if (!ws) return vegs_bin_count(tiles, n, offsets, kept_idx, counts, ws, ws_bytes, stream);
+    if (!step_state || !poison || inst_capacity < 0) return VEGS_ERR_ARG;
+    const int rc = vegs_bin_count(tiles, n, offsets, kept_idx, counts, ws, ws_bytes, stream);
+    if (rc != VEGS_OK) return rc;
+    cudaStream_t s = (cudaStream_t)stream;
+    capacity_check_kernel<<<1, 1, 0, s>>>(counts, inst_capacity, step_state, poison);
+    VEGS_CHECK_LAUNCH();
+    capacity_empty_kernel<<<(int)((n + 1 + 255) / 256), 256, 0, s>>>(poison, tiles, n, offsets, kept_idx);
+    VEGS_CHECK_LAUNCH();
+    return VEGS_OK;
+}
+
+extern "C" int vegs_bin_sort_dev(const uint64_t *depth_key, const int32_t *rect, const int64_t *offsets,
+                                 const int64_t *kept_idx, int64_t n, const int64_t *counts, int32_t width,
+                                 int32_t height, int32_t tile_size, uint32_t *sorted_gauss, int32_t *tile_start,
+                                 int32_t *tile_end, int32_t *tile_order, void *ws, size_t *ws_bytes, void *stream) {
+    if (!ws_bytes || tile_size != kTile || width < 1 || height < 1 || !counts) return VEGS_ERR_ARG;
+    if (n >= (int64_t(1) << 31)) return VEGS_ERR_ARG;
+    const int tiles_x = (width + kTile - 1) / kTile, tiles_y = (height + kTile - 1) / kTile;
+    if ((tiles_x + 1) * (tiles_y + 1) > kMaxPlaceTiles) return VEGS_ERR_ARG;  // radix path needs host counts
+    if (ws && (n > 0) && (!depth_key || !rect)) return VEGS_ERR_ARG;
+    if (ws && (!tile_start || !tile_end || !sorted_gauss)) return VEGS_ERR_ARG;
+    return bin_place_impl(depth_key, rect, offsets, kept_idx, n, n, 1, tiles_x, tiles_y, sorted_gauss, nullptr,
+                          nullptr, tile_start, tile_end, tile_order, ws, ws_bytes, (cudaStream_t)stream, counts);
 }

@@ -133,11 +133,16 @@ struct GradParts {
 
 __global__ void __launch_bounds__(256) adam_kernel(double *params, GradParts gp, double *m, double *v, int64_t n,
                                                    const double *lr, double grad_scale, double bias1, double bias2,
-                                                   int *nonfinite) {
+                                                   int *nonfinite, const int64_t *skip) {
+    if (skip && skip[0]) return;  // a view of the step overflowed its buffers: the step is redone
     const int unit = blockIdx.y;
     const int cls = kUnitClass[unit];
     const double b1 = 0.9, b2 = 0.999, eps = 1e-15;
     const double lr_c = params ? lr[cls] : 0.0;
+    if (bias1 != bias1) {  // NaN marks "from the device": lr[10], lr[11] hold 1 - beta^t (graph replay)
+        bias1 = lr[10];
+        bias2 = lr[11];
+    }
     const int64_t base = (int64_t)unit * n;
     for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x) {
         const int64_t i = base + j;
@@ -225,7 +230,8 @@ extern "C" int vegs_splat_table_from_arrays(const double *mean2d, const double *
 }
 
 static int adam_launch(double *params, GradParts gp, double *m, double *v, int64_t n, const double *lr,
-                       double grad_scale, double bias1, double bias2, int32_t *nonfinite, void *stream) {
+                       double grad_scale, double bias1, double bias2, int32_t *nonfinite, void *stream,
+                       const int64_t *skip = nullptr) {
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -233,7 +239,7 @@ static int adam_launch(double *params, GradParts gp, double *m, double *v, int64
     const int cap = (sms * 8 + 18) / 19;  // ~8 resident 256-thread CTAs per SM over the 19 units
     if (bx > cap) bx = cap;
     adam_kernel<<<dim3(bx, 19), 256, 0, (cudaStream_t)stream>>>(params, gp, m, v, n, lr, grad_scale, bias1, bias2,
-                                                                nonfinite);
+                                                                nonfinite, skip);
     VEGS_CHECK_LAUNCH();
     return VEGS_OK;
 }
@@ -248,16 +254,16 @@ extern "C" int vegs_adam_step(double *params, const double *grads, double *m, do
 }
 
 extern "C" int vegs_adam_step_sum(double *params, double *grads0, const double *grads1, const double *grads2,
-                                  const double *grads3, double *m, double *v, int64_t n, const double *lr,
-                                  double grad_scale, double bias1, double bias2, int32_t *nonfinite, void *stream) {
+                                  const double *grads3, double *m, double *v, int64_t n, const double *hyper,
+                                  double grad_scale, int32_t *nonfinite, const int64_t *skip, void *stream) {
     if (n > 0 && !grads0) return VEGS_ERR_ARG;
-    if (n > 0 && params && (!m || !v || !lr || !nonfinite)) return VEGS_ERR_ARG;
+    if (n > 0 && params && (!m || !v || !hyper || !nonfinite)) return VEGS_ERR_ARG;
     const double *extra[3] = {grads1, grads2, grads3};
     GradParts gp{grads0, {nullptr, nullptr, nullptr}, 0};
     for (int k = 0; k < 3; ++k)
         if (extra[k]) gp.g[gp.n_extra++] = extra[k];
     if (n == 0 || (!params && gp.n_extra == 0)) return VEGS_OK;
-    return adam_launch(params, gp, m, v, n, lr, grad_scale, bias1, bias2, nonfinite, stream);
+    return adam_launch(params, gp, m, v, n, hyper, grad_scale, NAN, NAN, nonfinite, stream, skip);
 }
 
 // ---------------------------------------------------------------------------------

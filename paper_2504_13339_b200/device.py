@@ -38,6 +38,8 @@ LAUNCHES = {
     "vegs_preprocess_forward": 1,
     "vegs_splat_table_from_arrays": 1,
     "vegs_bin_count": 4,          # pack, CUB scan (init + sweep), unpack
+    "vegs_bin_count_dev": 4,      # the same (+2 capacity-check launches counted in forward_end)
+    "vegs_bin_sort_dev": 18,      # the placement path of vegs_bin_sort
     "vegs_bin_sort": 18,          # counting placement: coarse keys, CUB depth sort (hist + scan + 4 onesweep), ties,
                                   # chunk counts, group sums, group scan, CUB scan (2), chunk offsets, placement,
                                   # tile weights + single-tile CUB sort (heaviest-first tile order); +1 (order /
@@ -209,6 +211,8 @@ class Frame:
     api: dict = field(default_factory=dict)
     visited: torch.Tensor | None = None  # per-instance bitmask of the latest backward_rows
     defer: torch.Tensor | None = None  # fast-T forward: [count, pixels re-blended in float64]
+    counts: torch.Tensor | None = None  # device (n_kept, n_inst)
+    counts_on_device: bool = False  # device-count binning: n_kept / n_inst above are the capacity
 
     @property
     def n_deferred(self) -> int:
@@ -247,6 +251,16 @@ class Rasterizer:
         # float32 blends: carry T in float32 with exact decisions (vegs_composite_forward_fast)
         # instead of the float64 chain that reproduces the reference's T bit for bit
         self.fast_t = fast_t
+        # device-count binning (set by the Trainer): an int64[2] step state shared by the
+        # views of a step and the instance capacity of this rasteriser's pooled buffers
+        self.device_counts: torch.Tensor | None = None
+        self.inst_cap = 0
+
+    @staticmethod
+    def _placement(width: int, height: int) -> bool:
+        """Counting placement (<= 12288 tiles, VEGS_BIN_RADIX unset) -- the C library's rule."""
+        tx, ty = (width + TILE - 1) // TILE, (height + TILE - 1) // TILE
+        return (tx + 1) * (ty + 1) <= 12288 and os.environ.get("VEGS_BIN_RADIX", "")[:1] in ("", "0")
 
     def _run(self, name: str, *args) -> None:
         if self.timer is not None:
@@ -314,6 +328,16 @@ class Rasterizer:
         s = _stream()
         wsz = _lib.size_query("vegs_bin_count", _p(tiles), n, _p(offsets), _p(kept_idx), _p(counts), tail=(s,))
         ws = A.get("ws_count", wsz, torch.uint8)
+        if self.device_counts is not None and not want_order and self._placement(width, height):
+            # counts stay on the device (no host round trip: CUDA-graph capturable); a view
+            # above the instance capacity is emptied and flagged in the step state
+            poison = A.get("poison", 1, torch.int32)
+            self._run("vegs_bin_count_dev", _p(tiles), n, _p(offsets), _p(kept_idx), _p(counts),
+                      int(self.inst_cap), _p(self.device_counts), _p(poison), _p(ws),
+                      ctypes.byref(ctypes.c_size_t(wsz)), s)
+            return dict(A=A, n=n, record=record, rect=rect, tiles=tiles, depth_key=depth_key, width=width,
+                        height=height, background=background, cs=cs, tf=tf, params=params, want_order=want_order,
+                        api=api, offsets=offsets, kept_idx=kept_idx, counts=counts, device=True)
         self._run("vegs_bin_count", _p(tiles), n, _p(offsets), _p(kept_idx), _p(counts), _p(ws),
              ctypes.byref(ctypes.c_size_t(wsz)), s)
         # pinned count buffer + event from a free list (a pinned allocation per view costs
@@ -335,28 +359,39 @@ class Rasterizer:
                                                                        "params"))
         want_order, api, offsets, kept_idx = pend["want_order"], pend["api"], pend["offsets"], pend["kept_idx"]
         s = _stream()
-        pend["event"].synchronize()
-        n_kept, n_inst = (int(x) for x in pend["host"].tolist())
-        self._count_slots.append(pend.pop("slot"))
-        self.last_counts = (n_kept, n_inst)
         tiles_x = (width + TILE - 1) // TILE
         n_tiles = tiles_x * ((height + TILE - 1) // TILE)
-        sorted_gauss = A.get("sorted_gauss", n_inst, torch.int32)
-        inst_pid = A.get("inst_pid", n_inst, torch.int32) if want_order else None
-        order = A.get("order", n_inst, torch.int64) if want_order else None
         tile_start = A.get("tile_start", n_tiles, torch.int32)
         tile_end = A.get("tile_end", n_tiles, torch.int32)
         tile_order = A.get("tile_order", n_tiles, torch.int32)
-        args = (_p(tiles), _p(depth_key), _p(rect), _p(offsets), _p(kept_idx), n, n_kept, n_inst, width, height,
-                TILE, _p(sorted_gauss), _p(inst_pid), _p(order), _p(tile_start), _p(tile_end), _p(tile_order))
-        wsz = _lib.size_query("vegs_bin_sort", *args, tail=(s,))
-        ws = A.get("ws_sort", wsz, torch.uint8)
-        self._run("vegs_bin_sort", *args, _p(ws), ctypes.byref(ctypes.c_size_t(wsz)), s)
-        if (tiles_x + 1) * ((height + TILE - 1) // TILE + 1) > 12288 or \
-                os.environ.get("VEGS_BIN_RADIX", "")[:1] not in ("", "0"):  # the C rule: set, not '0...'
-            self.launches += 1  # radix path
-        elif want_order:
-            self.launches += 1  # order / inst_pid for the reference-shaped API
+        inst_pid = order = None
+        if pend.get("device"):
+            # capacity-sized buffers, counts read by the kernels from the device
+            n_kept = n_inst = int(self.inst_cap)
+            sorted_gauss = A.get("sorted_gauss", n_inst, torch.int32)
+            args = (_p(depth_key), _p(rect), _p(offsets), _p(kept_idx), n, _p(pend["counts"]), width, height, TILE,
+                    _p(sorted_gauss), _p(tile_start), _p(tile_end), _p(tile_order))
+            wsz = _lib.size_query("vegs_bin_sort_dev", *args, tail=(s,))
+            ws = A.get("ws_sort", wsz, torch.uint8)
+            self._run("vegs_bin_sort_dev", *args, _p(ws), ctypes.byref(ctypes.c_size_t(wsz)), s)
+            self.launches += 2  # the capacity check of vegs_bin_count_dev
+        else:
+            pend["event"].synchronize()
+            n_kept, n_inst = (int(x) for x in pend["host"].tolist())
+            self._count_slots.append(pend.pop("slot"))
+            sorted_gauss = A.get("sorted_gauss", n_inst, torch.int32)
+            inst_pid = A.get("inst_pid", n_inst, torch.int32) if want_order else None
+            order = A.get("order", n_inst, torch.int64) if want_order else None
+            args = (_p(tiles), _p(depth_key), _p(rect), _p(offsets), _p(kept_idx), n, n_kept, n_inst, width, height,
+                    TILE, _p(sorted_gauss), _p(inst_pid), _p(order), _p(tile_start), _p(tile_end), _p(tile_order))
+            wsz = _lib.size_query("vegs_bin_sort", *args, tail=(s,))
+            ws = A.get("ws_sort", wsz, torch.uint8)
+            self._run("vegs_bin_sort", *args, _p(ws), ctypes.byref(ctypes.c_size_t(wsz)), s)
+            if not self._placement(width, height):
+                self.launches += 1  # radix path
+            elif want_order:
+                self.launches += 1  # order / inst_pid for the reference-shaped API
+        self.last_counts = (n_kept, n_inst)
         hw = width * height
         out_img = A.get("out_img", hw * self.n_ch, self.real)
         out_t = A.get("out_t", hw, self.real)
@@ -380,7 +415,8 @@ class Rasterizer:
                      depth_key=depth_key, offsets=offsets, kept_idx=kept_idx, n_kept=n_kept, n_inst=n_inst,
                      sorted_gauss=sorted_gauss, inst_pid=inst_pid, order=order, tile_start=tile_start,
                      tile_end=tile_end, tile_order=tile_order, out_img=out_img, out_t=out_t, out_last=out_last,
-                     n_contrib=n_contrib, api=api, defer=defer)
+                     n_contrib=n_contrib, api=api, defer=defer, counts=pend.get("counts"),
+                     counts_on_device=bool(pend.get("device")))
 
     # -- backward -------------------------------------------------------------------
     def backward_rows(self, fr: Frame, d_img: torch.Tensor, d_alpha: torch.Tensor | None = None) -> torch.Tensor:
@@ -482,8 +518,22 @@ def adam_step_device(params, grads, m, v, n: int, lrs: torch.Tensor, grad_scale:
              1.0 - b1 ** step, 1.0 - b2 ** step, _p(nonfinite), _stream())
         return
     ex = list(extra_grads) + [None] * (3 - len(extra_grads))
-    call("vegs_adam_step_sum", _p(params), _p(grads), _p(ex[0]), _p(ex[1]), _p(ex[2]), _p(m), _p(v), n, _p(lrs),
-         float(grad_scale), 1.0 - b1 ** step, 1.0 - b2 ** step, _p(nonfinite), _stream())
+    hyper = None
+    if params is not None:
+        hyper = torch.cat([lrs.to(torch.float64), torch.tensor([1.0 - b1 ** step, 1.0 - b2 ** step],
+                                                               dtype=torch.float64, device=lrs.device)])
+    call("vegs_adam_step_sum", _p(params), _p(grads), _p(ex[0]), _p(ex[1]), _p(ex[2]), _p(m), _p(v), n, _p(hyper),
+         float(grad_scale), _p(nonfinite), None, _stream())
+
+
+def adam_step_sum_device(params, grads, m, v, n: int, hyper: torch.Tensor, nonfinite: torch.Tensor, extra_grads=(),
+                         skip: torch.Tensor | None = None) -> None:
+    """The trainer's Adam: ``hyper`` (device, 12 float64: lr per class, 1 - beta1^t,
+    1 - beta2^t) is read at execution time (graph replay); ``skip`` (device int64) set by an
+    overflowed view leaves everything unchanged."""
+    ex = list(extra_grads) + [None] * (3 - len(extra_grads))
+    call("vegs_adam_step_sum", _p(params), _p(grads), _p(ex[0]), _p(ex[1]), _p(ex[2]), _p(m), _p(v), n, _p(hyper),
+         1.0, _p(nonfinite), _p(skip), _stream())
 
 
 class RenderPipeline:

@@ -23,7 +23,7 @@ import numpy as np
 import torch
 
 from .constants import DEFAULT_SETTINGS, RasterSettings
-from .device import DeviceTF, Rasterizer, adam_step_device, require_cuda, use_stream
+from .device import DeviceTF, Rasterizer, adam_step_device, adam_step_sum_device, require_cuda, use_stream
 from .model import PARAM_CLASSES, GaussianSet, class_offsets
 from .parallel import allreduce_gradients
 
@@ -176,6 +176,7 @@ class _Lane:
         self.d_img = None
         self.grads = None
         self.dstats = None
+        self.dstats_saved = None  # device-count steps: dstats before the step (restored on overflow)
 
     def prepare(self, tr: "Trainer") -> None:
         if self.grads is None or self.grads.numel() != tr.params.numel():
@@ -186,6 +187,7 @@ class _Lane:
             self.dstats = torch.zeros_like(tr.densify_stats)
 
 
+
 class Trainer:
     """Multi-view training step on device-resident float64 parameters.
 
@@ -194,7 +196,7 @@ class Trainer:
 
     def __init__(self, gs: GaussianSet, config: TrainConfig, settings: RasterSettings = DEFAULT_SETTINGS,
                  background=(1.0, 1.0, 1.0), l1_weight: float | None = None, group=None, with_aux: bool = False,
-                 lanes: int = 4, fast_t: bool = False):
+                 lanes: int = 4, fast_t: bool = False, graphs: bool = False):
         self.device = require_cuda()
         # fast_t: the forward carries T in float32 with every skip / clamp / termination
         # decision exact (vegs_composite_forward_fast).  Default: the float64 chain, which
@@ -228,6 +230,25 @@ class Trainer:
         # the H2D copies overlap the previous views' compositing
         self._copy_stream = None
         self._target_bufs: list[torch.Tensor] = []
+        # Adam's per-step constants: pinned host buffer -> device buffer on every step
+        self._hyper_host = torch.zeros(12, dtype=torch.float64, pin_memory=True)
+        self._hyper_dev = torch.zeros(12, dtype=torch.float64, device=self.device)
+        # graphs=True: device-count binning + one CUDA graph per set of views (see step)
+        self._graphs: dict = {}
+        self._graph_pool = None
+        self._state = torch.zeros(2, dtype=torch.int64, device=self.device)  # [overflow, max instances]
+        self._state_host = torch.zeros(2, dtype=torch.int64, pin_memory=True)
+        self._state_event = torch.cuda.Event()
+        self.set_graphs(graphs)
+
+    def set_graphs(self, on: bool) -> None:
+        """Switch between device-count steps captured as CUDA graphs (on) and host-counted
+        eager steps (off: per-view instance counts on the host, e.g. for per-kernel events)."""
+        self.graphs = on
+        if on and self._graph_pool is None:
+            self._graph_pool = torch.cuda.graph_pool_handle()
+        for lane in self.lanes:
+            lane.rz.device_counts = self._state if on else None
 
     def set_timer(self, timer) -> None:
         for lane in self.lanes:
@@ -293,9 +314,37 @@ class Trainer:
     def step(self, views: list[View], total_views: int | None = None, iteration: int | None = None,
              scene_extent: float = 1.0) -> torch.Tensor:
         """One optimisation step over this rank's views; returns the mean loss over
-        this rank's views as a device scalar (no host sync besides the per-view counts)."""
-        main = torch.cuda.current_stream(self.device)
+        this rank's views as a device scalar.
+
+        Default (``graphs=False``): views are enqueued with one host read of each view's
+        instance count (it sizes the view's buffers).  ``graphs=True``: the counts stay on the
+        device (capacity-sized buffers, ``vegs_bin_count_dev``), so a whole step -- every view
+        on every lane, the lane sum, the all-reduce, Adam -- is captured once per set of views
+        as a CUDA graph and replayed; the host waits once per step, for the overflow check."""
         total = total_views if total_views is not None else len(views)
+        self.step_count += 1
+        it = self.step_count if iteration is None else iteration
+        lrs = learning_rates(self.config, it, scene_extent)
+        if self.graphs:
+            return self._step_device(views, total, lrs)
+        hyper = self._hyper(lrs)
+        return self._step_body(views, total, hyper, None)
+
+    def _hyper(self, lrs: dict) -> torch.Tensor:
+        """[lr per class (10), 1 - beta1^t, 1 - beta2^t] in the pinned host buffer, copied to
+        the device on the current stream (a graph copies it at replay time)."""
+        t = self.step_count
+        hh = self._hyper_host
+        hh[:10] = torch.tensor([lrs[k] for k in PARAM_CLASSES], dtype=torch.float64)
+        hh[10] = 1.0 - ADAM_BETA1 ** t
+        hh[11] = 1.0 - ADAM_BETA2 ** t
+        return self._hyper_dev
+
+    def _step_body(self, views: list[View], total: int, hyper: torch.Tensor, state) -> torch.Tensor:
+        main = torch.cuda.current_stream(self.device)
+        self._hyper_dev.copy_(self._hyper_host, non_blocking=True)
+        if state is not None:
+            state.zero_()
         n_v = len(views)
         sums = torch.zeros(n_v, 5, dtype=torch.float64, device=self.device)
         lanes = self.lanes
@@ -306,6 +355,12 @@ class Trainer:
             lanes[0].stream.wait_stream(main)
         lanes[0].grads = self.grads
         lanes[0].dstats = self.densify_stats
+        if state is not None and self.densify_stats is not None:  # restored if the step overflows
+            for lane in lanes:
+                if lane.dstats is not None:
+                    if lane.dstats_saved is None or lane.dstats_saved.numel() != lane.dstats.numel():
+                        lane.dstats_saved = torch.empty_like(lane.dstats)
+                    lane.dstats_saved.copy_(lane.dstats)
         targets = self._upload_targets(views, main)
         pend: list = [None] * n_v
         used = [False] * len(lanes)
@@ -345,11 +400,10 @@ class Trainer:
             adam_step_device(None, self.grads, None, None, self.n, None, 1.0, 1, None, extra[:3])
             extra = extra[3:]
         allreduce_gradients(self.grads, self.group)
-        self.step_count += 1
-        it = self.step_count if iteration is None else iteration
-        lrs = _lr_tensor(learning_rates(self.config, it, scene_extent), self.device)
-        adam_step_device(self.params, self.grads, self.m, self.v, self.n, lrs, 1.0, self.step_count,
-                         self.nonfinite, extra)
+        adam_step_sum_device(self.params, self.grads, self.m, self.v, self.n, hyper, self.nonfinite, extra,
+                             skip=state)
+        if state is not None:
+            self._state_host.copy_(state, non_blocking=True)
         if not views:
             return torch.zeros((), dtype=torch.float64, device=self.device)
         # per-view normalisers (views may differ in resolution): element count, valid SSIM
@@ -370,6 +424,53 @@ class Trainer:
                                               torch.zeros_like(cnt))
             per_view = per_view + self.config.smooth_loss_weight * sums[:, 4] / n_pair
         return per_view.mean()
+
+    def _graph_key(self, views: list[View], total: int):
+        return (tuple((id(v.camera), id(v.tf), id(v.target)) for v in views), total, self.n,
+                self.densify_stats is not None, torch.cuda.current_stream(self.device).cuda_stream)
+
+    def _step_device(self, views: list[View], total: int, lrs: dict) -> torch.Tensor:
+        """Device-count step: replay the captured graph of these views (capture it after the
+        first eager run), then one host wait for the step state; a view that overflowed its
+        instance capacity left the parameters untouched (Adam skipped), so the buffers grow
+        and the step is redone."""
+        self._hyper(lrs)
+        key = self._graph_key(views, total)
+        uniform = len({(int(v.camera.height), int(v.camera.width)) for v in views}) <= 1
+        for _ in range(8):
+            entry = self._graphs.get(key)
+            if entry is not None:
+                entry[0].replay()
+                loss = entry[1]
+            else:
+                loss = self._step_body(views, total, self._hyper_dev, self._state)
+            self._state_event.record(torch.cuda.current_stream(self.device))
+            self._state_event.synchronize()
+            if not int(self._state_host[0]):
+                if entry is None and uniform and views:
+                    self._capture(key, views, total)
+                return loss
+            # overflow: grow every lane's capacity to the largest view seen, forget the graphs
+            # (their buffers are the old size), restore the densify statistics, redo the step
+            cap = int(int(self._state_host[1]) * 1.25) + 4096
+            for lane in self.lanes:
+                lane.rz.inst_cap = max(lane.rz.inst_cap, cap)
+                if self.densify_stats is not None and lane.dstats is not None:
+                    lane.dstats.copy_(lane.dstats_saved)
+            self._graphs.clear()
+        raise RuntimeError("instance capacity did not converge")
+
+    def _capture(self, key, views: list[View], total: int) -> None:
+        main = torch.cuda.current_stream(self.device)
+        cap_stream = torch.cuda.Stream(self.device)
+        cap_stream.wait_stream(main)
+        g = torch.cuda.CUDAGraph()
+        lane0 = self.lanes[0].stream
+        with torch.cuda.graph(g, stream=cap_stream, pool=self._graph_pool):
+            loss = self._step_body(views, total, self._hyper_dev, self._state)
+        main.wait_stream(cap_stream)
+        assert self.lanes[0].stream is lane0
+        self._graphs[key] = (g, loss)
 
     def track_densify(self, on: bool = True) -> None:
         """Accumulate DensifyStats (per view, fused into the backward) from now on."""
@@ -402,6 +503,7 @@ class Trainer:
         p, m, v, n_out = densify_device(self.params, self.m, self.v, self.n, self.densify_stats, self.config,
                                         scene_extent, rng, position_lr, mo, max_gaussians)
         self.params, self.m, self.v, self.n = p.clone(), m.clone(), v.clone(), n_out
+        self._graphs.clear()  # captured with the old buffers
         self.grads = torch.zeros_like(self.params)
         self.densify_stats = torch.zeros(self.n * 5, dtype=torch.float64, device=self.device)
         return n_out

@@ -485,3 +485,64 @@ def test_c2_single_entry_forward_vs_reference(monkeypatch, c2_ref):
     assert np.array_equal(digest(fr.out_last.cpu().numpy().astype(np.int64), np.int64), d["out_last_sha"])
     assert np.array_equal(digest(fr.n_contrib.cpu().numpy(), np.int32), d["n_contrib_sha"])
     assert np.array_equal(digest(fr.out_t.cpu().numpy(), np.float32), d["out_t_sha"])
+
+
+# -- device-count steps captured as CUDA graphs ---------------------------------------------
+
+def _graph_runs(views_fn, steps, lanes=4, **kw):
+    learned = scenes.random_gaussians(2000, seed=0)
+    out = {}
+    for graphs in (False, True):
+        tr = Trainer(learned, TrainConfig(iterations=100), lanes=lanes, graphs=graphs, **kw)
+        losses = [float(tr.step(views_fn(s), iteration=s + 1).item()) for s in range(steps)]
+        torch.cuda.synchronize()
+        out[graphs] = (losses, tr.params.clone(), tr.grads.clone(), tr)
+    return out
+
+
+def test_graph_steps_bitwise_equal_eager_steps():
+    """graphs=True (device-side instance counts, capacity-sized buffers, one captured CUDA
+    graph per set of views, replayed) gives bitwise the eager host-counted steps: the first
+    step overflows the empty capacity, is redone, then the graph is captured and replayed."""
+    learned, dtf, cams, targets = _train_scene(5)
+    views = [View(c, dtf, t) for c, t in zip(cams, targets)]
+    res = _graph_runs(lambda s: views, 4)
+    (le, pe, ge, _), (lg, pg, gg, tr) = res[False], res[True]
+    assert le == lg
+    assert torch.equal(pe, pg) and torch.equal(ge, gg)
+    assert len(tr._graphs) == 1 and all(l.rz.inst_cap > 0 for l in tr.lanes)
+
+
+def test_graph_steps_with_alternating_views_and_host_targets():
+    """Two alternating sets of views (two cached graphs), pinned host targets uploaded inside
+    the graph, and DensifyStats tracking: bitwise the eager run."""
+    learned, dtf, cams, targets = _train_scene(4)
+    dtf2 = DeviceTF(scenes.random_tf(5, 3))
+    host = [t.cpu().pin_memory() for t in targets]
+    sets = [[View(c, dtf, t) for c, t in zip(cams, host)], [View(c, dtf2, t) for c, t in zip(cams[:3], host[:3])]]
+    out = {}
+    for graphs in (False, True):
+        tr = Trainer(learned, TrainConfig(iterations=100), graphs=graphs)
+        tr.track_densify()
+        losses = [float(tr.step(sets[s % 2], iteration=s + 1, total_views=4).item()) for s in range(6)]
+        st = tr.gather_densify_stats().clone()
+        out[graphs] = (losses, tr.params.clone(), st)
+        if graphs:
+            assert len(tr._graphs) == 2
+    assert out[False][0] == out[True][0]
+    assert torch.equal(out[False][1], out[True][1]) and torch.equal(out[False][2], out[True][2])
+
+
+def test_graph_step_overflow_regrows_and_redoes():
+    """A view with more instances than the captured capacity: the step is emptied on the
+    device, Adam skips, the host grows the buffers and redoes it -- same parameters as eager."""
+    learned, dtf, cams, targets = _train_scene(3)
+    views = [View(c, dtf, t) for c, t in zip(cams, targets)]
+    big = scenes.orbit_cameras(1, 9, 160, 128)[0]
+    rz = Rasterizer(pooled=False)
+    truth = torch.from_numpy(scenes.random_gaussians(2000, seed=1).pack()).cuda()
+    tbig = rz.forward(truth, 2000, dtf, big).out_img.view(128, 160, 3).clone()
+    views2 = views + [View(big, dtf, tbig)]
+    res = _graph_runs(lambda s: views if s < 2 else views2, 4)
+    assert res[False][0] == res[True][0]
+    assert torch.equal(res[False][1], res[True][1])
