@@ -68,19 +68,25 @@ def parse():
     ap.add_argument("--c4-steps", type=int, default=20)
     ap.add_argument("--sweep-frames", type=int, default=2)
     ap.add_argument("--lanes", type=int, default=4, help="CUDA-stream lanes of the view pipeline")
+    ap.add_argument("--no-graphs", action="store_true",
+                    help="host-counted eager steps instead of device-count steps replayed as CUDA graphs")
     ap.add_argument("--backend", choices=("nccl", "gloo"), default="nccl",
                     help="gradient all-reduce backend for N>1 (gloo: host-side plumbing check only)")
     return ap.parse_args()
 
 
-def config_block(world: int, backend: str = "nccl") -> dict:
-    return {"workload": "c2: 1M Gaussians (seed 0) fit to renders of a 1M-Gaussian 64-blob set (seed 1); "
+def config_block(world: int, backend: str = "nccl", graphs: bool | None = True) -> dict:
+    cfg = {"workload": "c2: 1M Gaussians (seed 0) fit to renders of a 1M-Gaussian 64-blob set (seed 1); "
                         "16 views/step at 1024x1024, 256-knot TF; step = render + L1/SSIM + backward "
                         "+ all-reduce + Adam",
             "n_gaussians": 1_000_000, "views_per_step": VIEWS_PER_STEP, "width": 1024, "height": 1024,
             "loss": "0.8*L1 + 0.2*(1-SSIM) (reference (1-lambda) weighting)",
             "parallelism": f"view-sharded dp{world}" + ("" if world == 1 or backend == "nccl" else f" ({backend})"),
             "l2": "inputs larger than L2 (no flush needed)"}
+    if graphs is not None:
+        cfg["step_execution"] = ("device-side instance counts, each step one replayed CUDA graph (all views, lanes, "
+                                 "Adam); one host wait per step" if graphs else "eager, one host count read per view")
+    return cfg
 
 
 def peaks() -> tuple[float, str]:
@@ -273,7 +279,8 @@ def run_b200(args) -> None:
     torch.cuda.synchronize()
 
     group = dist.group.WORLD if world > 1 else None
-    trainer = Trainer(learned, TrainConfig(iterations=30000), group=group, lanes=args.lanes)
+    trainer = Trainer(learned, TrainConfig(iterations=30000), group=group, lanes=args.lanes,
+                      graphs=not args.no_graphs)
     views = [View(cams[i], dtf, targets[j]) for j, i in enumerate(mine)]
 
     def barrier():
@@ -318,6 +325,8 @@ def run_b200(args) -> None:
     # host-side event records would perturb it)
     timer = KernelTimer(trainer.rz)
     trainer.set_timer(timer)
+    trainer.set_graphs(False)  # eager, host-counted launches: events around each kernel, live counts
+    trainer.step(views, total_views=VIEWS_PER_STEP)
     k_steps = max(min(args.steps, 5), 2)
     torch.cuda.synchronize()
     t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -327,7 +336,9 @@ def run_b200(args) -> None:
     t1.record()
     torch.cuda.synchronize()
     trainer.set_timer(None)
+    trainer.set_graphs(not args.no_graphs)
     ktimed_ms = t0.elapsed_time(t1)
+    timer.done = {k: v[len(v) // (k_steps + 1):] for k, v in timer.done.items()}  # drop the re-warm step
     ksum = timer.summary()
 
     # ---- per-stage profile, serialised on one stream (the pipelined step overlaps stages,
@@ -481,7 +492,7 @@ def run_b200(args) -> None:
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": max(args.warmup, 3), "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f32+f64", "data": "synthetic (seeded, scenes.py)",
-            "config": config_block(world, args.backend), "e2e": e2e, "render_mpx_s": render_mpx_s,
+            "config": config_block(world, args.backend, not args.no_graphs), "e2e": e2e, "render_mpx_s": render_mpx_s,
             "render_roofline": render_roof, "loss": loss_val,
             "gpu_launches": int(launches), "roofline": roof, "kernels": kernels, "stages": stages,
             "render_sweep_c3": sweep,
@@ -626,14 +637,15 @@ def run_c4(args, dev, rank, world) -> dict:
             targets[(k, i)] = fr.out_img.view(cams[i].height, cams[i].width, 3).clone()
     del rz, gt
     group = dist.group.WORLD if world > 1 else None
-    tr = Trainer(learned, TrainConfig(iterations=30000), group=group)
+    tr = Trainer(learned, TrainConfig(iterations=30000), group=group, graphs=not args.no_graphs)
     tr.track_densify(True)
+    view_sets = {k: [View(cams[i], tfs[k], targets[(k, i)]) for i in mine] for k in sorted(set(used))}
 
     def views_for(s):
-        k = used[s]
-        return [View(cams[i], tfs[k], targets[(k, i)]) for i in mine]
+        return view_sets[used[s]]
 
-    tr.step(views_for(0), total_views=len(cams))  # warm-up
+    for k in sorted(set(used)):  # warm-up: every TF's view set once (and its graph captured)
+        tr.step(view_sets[k], total_views=len(cams))
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
@@ -806,7 +818,7 @@ def run_reference(args) -> None:
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
             "steps": 1 if full else 0, "warmup": 0, "ms_per_step": step_s * 1000.0, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64 (f32 blend planes)", "data": "synthetic (seeded)",
-            "config": config_block(1), "views_timed": k, "extrapolated": not full,
+            "config": config_block(1, graphs=None), "views_timed": k, "extrapolated": not full,
             "view_s": view_s, "adam_s": adam_s, "jit_warmup_s": jit_s,
             "reference": {"package": "vegsplat 0.1.0 (baseline/_ref, unmodified)", "numba": numba.__version__,
                           "numba_threads": threads, "host_cpus": os.cpu_count()},

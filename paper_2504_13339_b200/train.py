@@ -236,6 +236,7 @@ class Trainer:
         # graphs=True: device-count binning + one CUDA graph per set of views (see step)
         self._graphs: dict = {}
         self._graph_pool = None
+        self._replayed_launches = 0
         self._state = torch.zeros(2, dtype=torch.int64, device=self.device)  # [overflow, max instances]
         self._state_host = torch.zeros(2, dtype=torch.int64, pin_memory=True)
         self._state_event = torch.cuda.Event()
@@ -257,7 +258,8 @@ class Trainer:
 
     @property
     def launches(self) -> int:
-        return sum(lane.rz.launches + lane.loss_launches for lane in self.lanes)
+        """Kernels launched by this trainer's steps (graph replays count their captured kernels)."""
+        return sum(lane.rz.launches + lane.loss_launches for lane in self.lanes) + self._replayed_launches
 
     def gaussians(self) -> GaussianSet:
         return GaussianSet.unpack(self.params.cpu().numpy(), self.n)
@@ -442,6 +444,7 @@ class Trainer:
             if entry is not None:
                 entry[0].replay()
                 loss = entry[1]
+                self._replayed_launches += entry[2]
             else:
                 loss = self._step_body(views, total, self._hyper_dev, self._state)
             self._state_event.record(torch.cuda.current_stream(self.device))
@@ -465,12 +468,13 @@ class Trainer:
         cap_stream = torch.cuda.Stream(self.device)
         cap_stream.wait_stream(main)
         g = torch.cuda.CUDAGraph()
-        lane0 = self.lanes[0].stream
+        before = sum(lane.rz.launches + lane.loss_launches for lane in self.lanes)
         with torch.cuda.graph(g, stream=cap_stream, pool=self._graph_pool):
             loss = self._step_body(views, total, self._hyper_dev, self._state)
         main.wait_stream(cap_stream)
-        assert self.lanes[0].stream is lane0
-        self._graphs[key] = (g, loss)
+        captured = sum(lane.rz.launches + lane.loss_launches for lane in self.lanes) - before
+        self._replayed_launches -= captured  # the capture itself launched nothing; replays count them
+        self._graphs[key] = (g, loss, captured)
 
     def track_densify(self, on: bool = True) -> None:
         """Accumulate DensifyStats (per view, fused into the backward) from now on."""
