@@ -151,21 +151,23 @@ int vegs_bin_sort(const uint32_t *tiles, const uint64_t *depth_key, const int32_
                   size_t *ws_bytes, void *stream);
 
 /* Device-count binning (no host round trip per view; CUDA-graph capturable).
- * vegs_bin_count_dev = vegs_bin_count, then: step_state[1] = max(step_state[1], n_instances);
- * if n_instances > inst_capacity the view is emptied (counts, tiles, offsets zeroed: every
- * later stage of the view runs on nothing, inside its buffers), *poison = 1 and
- * step_state[0] = 1 (the caller grows its buffers and redoes the step; the trainer's Adam
- * skips on it).  tiles is therefore read-write.  Same ws as vegs_bin_count.
+ * vegs_bin_count_dev = vegs_bin_count, then: step_state[1] = max(step_state[1], n_instances),
+ * step_state[2] = max(step_state[2], n_kept); if n_instances > inst_capacity or n_kept >
+ * kept_capacity the view is emptied (counts, tiles, offsets zeroed: every later stage of
+ * the view runs on nothing, inside its buffers), *poison = 1 and step_state[0] = 1 (the
+ * caller grows its capacities and redoes the step; the trainer's Adam skips on it).  tiles
+ * is therefore read-write.  Same ws as vegs_bin_count.
  * vegs_bin_sort_dev = vegs_bin_sort's counting placement with n_kept read from counts
- * (device); launches and the workspace are sized for n kept splats.  Views above 12288
- * tiles need the radix path and host counts: VEGS_ERR_ARG. */
+ * (device); launches and the workspace are sized for kept_capacity kept splats.  Views
+ * above 12288 tiles need the radix path and host counts: VEGS_ERR_ARG. */
 int vegs_bin_count_dev(uint32_t *tiles, int64_t n, int64_t *offsets, int64_t *kept_idx, int64_t *counts,
-                       int64_t inst_capacity, int64_t *step_state, int32_t *poison, void *ws,
-                       size_t *ws_bytes, void *stream);
+                       int64_t inst_capacity, int64_t kept_capacity, int64_t *step_state, int32_t *poison,
+                       void *ws, size_t *ws_bytes, void *stream);
 int vegs_bin_sort_dev(const uint64_t *depth_key, const int32_t *rect, const int64_t *offsets,
-                      const int64_t *kept_idx, int64_t n, const int64_t *counts, int32_t width,
-                      int32_t height, int32_t tile_size, uint32_t *sorted_gauss, int32_t *tile_start,
-                      int32_t *tile_end, int32_t *tile_order, void *ws, size_t *ws_bytes, void *stream);
+                      const int64_t *kept_idx, int64_t n, const int64_t *counts, int64_t kept_capacity,
+                      int32_t width, int32_t height, int32_t tile_size, uint32_t *sorted_gauss,
+                      int32_t *tile_start, int32_t *tile_end, int32_t *tile_order, void *ws,
+                      size_t *ws_bytes, void *stream);
 
 /* ---- composite -------------------------------------------------------------------- */
 /* Tile blend on the splat table.  out_img H x W x C, out_t H x W (storage type),

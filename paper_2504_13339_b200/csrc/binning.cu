@@ -68,6 +68,30 @@ __global__ void depth_key32_kernel(const uint64_t *key64, int64_t n, uint32_t *k
     ids[i] = (uint32_t)i;
 }
 
+// Device-count binning: the same coarse keys, compacted to the kept splats (kept_idx is the
+// kept-index scan, so index order survives and the stable sort below gives the same order
+// as sorting all n), padded with max keys up to the kept capacity: the sort then runs over
+// the kept capacity instead of every Gaussian (config 4: 8k kept of 200k).
+__global__ void depth_key32_compact_kernel(const uint64_t *key64, const int64_t *kept_idx, int64_t n,
+                                           int64_t kept_cap, const int64_t *n_kept_dev, uint32_t *key32,
+                                           uint32_t *ids) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t n_kept = *n_kept_dev;
+    if (i >= n_kept && i < kept_cap) {  // padding (sorts last, never read)
+        key32[i] = 0xffffffffu;
+        ids[i] = 0u;
+    }
+    if (i >= n) return;
+    const uint64_t k = key64[i];
+    if (k == ~0ull) return;  // culled
+    const int64_t pos = kept_idx[i];
+    if (pos >= kept_cap) return;  // (an emptied view: never read)
+    const uint64_t b = (k >> 63) ? (k & 0x7fffffffffffffffull) : ~k;
+    const uint32_t f = __float_as_uint((float)__longlong_as_double((long long)b));
+    key32[pos] = (f >> 31) ? ~f : (f | 0x80000000u);
+    ids[pos] = (uint32_t)i;
+}
+
 // Runs of equal coarse keys among the kept splats are re-ordered by the exact float64 key
 // (insertion sort, strict comparison: the stable sort's index order survives among equal
 // float64 depths).  Runs are almost always of length 1-2.
@@ -355,14 +379,17 @@ __global__ void placed_extras_kernel(const uint32_t *sorted_gauss, const int4 *r
 }
 
 // Device-count binning (graph capture: no host round trip for the counts).  A view whose
-// instance count exceeds the caller's capacity is turned into an empty view: its counts,
-// tile counts and offsets are zeroed, so every later stage of the view (sort, compositing,
-// backward) runs on nothing and stays inside its buffers; step_state records the overflow
-// ([0] = 1) and the largest count seen ([1]) for the caller to grow its buffers and redo.
-__global__ void capacity_check_kernel(int64_t *counts, int64_t capacity, int64_t *step_state, int32_t *poison) {
-    const int64_t n_inst = counts[1];
+// instance or kept-splat count exceeds the caller's capacities is turned into an empty
+// view: its counts, tile counts and offsets are zeroed, so every later stage of the view
+// (sort, compositing, backward) runs on nothing and stays inside its buffers; step_state
+// records the overflow ([0] = 1) and the largest counts seen ([1] instances, [2] kept
+// splats) for the caller to grow its capacities and redo.
+__global__ void capacity_check_kernel(int64_t *counts, int64_t capacity, int64_t kept_capacity, int64_t *step_state,
+                                      int32_t *poison) {
+    const int64_t n_kept = counts[0], n_inst = counts[1];
     atomicMax(reinterpret_cast<unsigned long long *>(step_state + 1), (unsigned long long)n_inst);
-    const bool over = n_inst > capacity;
+    atomicMax(reinterpret_cast<unsigned long long *>(step_state + 2), (unsigned long long)n_kept);
+    const bool over = n_inst > capacity || n_kept > kept_capacity;
     *poison = over ? 1 : 0;
     if (over) {
         atomicExch(reinterpret_cast<unsigned long long *>(step_state), 1ull);
@@ -532,10 +559,8 @@ static int bin_place_impl(const uint64_t *depth_key, const int32_t *rect, const 
     // counts_dev (device-count binning): n_kept / n_inst live on the device; every launch is
     // sized for n kept splats and the kernels read the real count (no host sync)
     const int64_t *n_kept_dev = counts_dev;
-    if (counts_dev) {
-        n_kept = n;
-        n_inst = 1;  // unknown on the host; only its zero test below matters
-    }
+    if (counts_dev) n_inst = 1;  // n_kept: the caller's kept capacity; n_inst only meets the zero test below
+    const int64_t n_sort = counts_dev ? n_kept : n;  // keys sorted: all n, or the compacted kept capacity
     const int n_tiles = tiles_x * tiles_y;
 #ifndef VEGS_PLACE_CHUNKS
 #define VEGS_PLACE_CHUNKS 2048
@@ -550,7 +575,7 @@ static int bin_place_impl(const uint64_t *depth_key, const int32_t *rect, const 
     size_t t_depth = 0, t_scan = 0, t_tiles = 0;
     {
         cub::DoubleBuffer<uint32_t> dk(nullptr, nullptr), dv(nullptr, nullptr);
-        VEGS_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, t_depth, dk, dv, (int64_t)n, 0, 32, s));
+        VEGS_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, t_depth, dk, dv, n_sort, 0, 32, s));
         uint32_t *u = nullptr;
         int32_t *v = nullptr;
         VEGS_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, t_scan, u, v, n_tiles, s));
@@ -581,16 +606,22 @@ static int bin_place_impl(const uint64_t *depth_key, const int32_t *rect, const 
     void *tmp = w;
     const size_t tb0 = align_up(t_max);
 
-    if (n_inst == 0) {
+    if (n_inst == 0 || n_kept == 0) {  // (device counts: a zero kept capacity -- the first, overflowing step)
         VEGS_CUDA(cudaMemsetAsync(tile_start, 0, sizeof(int32_t) * n_tiles, s));
         VEGS_CUDA(cudaMemsetAsync(tile_end, 0, sizeof(int32_t) * n_tiles, s));
     } else {
         // 1. stable depth order of the kept splats (as in bin_sort_impl)
-        depth_key32_kernel<<<(int)((n + 255) / 256), 256, 0, s>>>(depth_key, n, dk0, id0);
+        if (counts_dev) {
+            const int64_t m = n > n_sort ? n : n_sort;
+            depth_key32_compact_kernel<<<(int)((m + 255) / 256), 256, 0, s>>>(depth_key, kept_idx, n, n_sort,
+                                                                              n_kept_dev, dk0, id0);
+        } else {
+            depth_key32_kernel<<<(int)((n + 255) / 256), 256, 0, s>>>(depth_key, n, dk0, id0);
+        }
         VEGS_CHECK_LAUNCH();
         cub::DoubleBuffer<uint32_t> dk(dk0, dk1), dv(id0, id1);
         size_t tb = tb0;
-        VEGS_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tb, dk, dv, (int64_t)n, 0, 32, s));
+        VEGS_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tb, dk, dv, n_sort, 0, 32, s));
         depth_ties_kernel<<<(int)((n_kept + 255) / 256), 256, 0, s>>>(dk.Current(), depth_key, n_kept, dv.Current(),
                                                                      n_kept_dev);
         VEGS_CHECK_LAUNCH();
@@ -665,14 +696,14 @@ extern "C" int vegs_bin_sort(const uint32_t *tiles, const uint64_t *depth_key, c
 }
 
 extern "C" int vegs_bin_count_dev(uint32_t *tiles, int64_t n, int64_t *offsets, int64_t *kept_idx, int64_t *counts,
-                                  int64_t inst_capacity, int64_t *step_state, int32_t *poison, void *ws,
-                                  size_t *ws_bytes, void *stream) {
+                                  int64_t inst_capacity, int64_t kept_capacity, int64_t *step_state, int32_t *poison,
+                                  void *ws, size_t *ws_bytes, void *stream) {
     if (!ws) return vegs_bin_count(tiles, n, offsets, kept_idx, counts, ws, ws_bytes, stream);
-    if (!step_state || !poison || inst_capacity < 0) return VEGS_ERR_ARG;
+    if (!step_state || !poison || inst_capacity < 0 || kept_capacity < 0) return VEGS_ERR_ARG;
     const int rc = vegs_bin_count(tiles, n, offsets, kept_idx, counts, ws, ws_bytes, stream);
     if (rc != VEGS_OK) return rc;
     cudaStream_t s = (cudaStream_t)stream;
-    capacity_check_kernel<<<1, 1, 0, s>>>(counts, inst_capacity, step_state, poison);
+    capacity_check_kernel<<<1, 1, 0, s>>>(counts, inst_capacity, kept_capacity, step_state, poison);
     VEGS_CHECK_LAUNCH();
     capacity_empty_kernel<<<(int)((n + 1 + 255) / 256), 256, 0, s>>>(poison, tiles, n, offsets, kept_idx);
     VEGS_CHECK_LAUNCH();
@@ -680,15 +711,17 @@ extern "C" int vegs_bin_count_dev(uint32_t *tiles, int64_t n, int64_t *offsets, 
 }
 
 extern "C" int vegs_bin_sort_dev(const uint64_t *depth_key, const int32_t *rect, const int64_t *offsets,
-                                 const int64_t *kept_idx, int64_t n, const int64_t *counts, int32_t width,
-                                 int32_t height, int32_t tile_size, uint32_t *sorted_gauss, int32_t *tile_start,
-                                 int32_t *tile_end, int32_t *tile_order, void *ws, size_t *ws_bytes, void *stream) {
+                                 const int64_t *kept_idx, int64_t n, const int64_t *counts, int64_t kept_capacity,
+                                 int32_t width, int32_t height, int32_t tile_size, uint32_t *sorted_gauss,
+                                 int32_t *tile_start, int32_t *tile_end, int32_t *tile_order, void *ws,
+                                 size_t *ws_bytes, void *stream) {
     if (!ws_bytes || tile_size != kTile || width < 1 || height < 1 || !counts) return VEGS_ERR_ARG;
     if (n >= (int64_t(1) << 31)) return VEGS_ERR_ARG;
     const int tiles_x = (width + kTile - 1) / kTile, tiles_y = (height + kTile - 1) / kTile;
     if ((tiles_x + 1) * (tiles_y + 1) > kMaxPlaceTiles) return VEGS_ERR_ARG;  // radix path needs host counts
     if (ws && (n > 0) && (!depth_key || !rect)) return VEGS_ERR_ARG;
     if (ws && (!tile_start || !tile_end || !sorted_gauss)) return VEGS_ERR_ARG;
-    return bin_place_impl(depth_key, rect, offsets, kept_idx, n, n, 1, tiles_x, tiles_y, sorted_gauss, nullptr,
+    const int64_t kc = kept_capacity < n ? kept_capacity : n;
+    return bin_place_impl(depth_key, rect, offsets, kept_idx, n, kc, 1, tiles_x, tiles_y, sorted_gauss, nullptr,
                           nullptr, tile_start, tile_end, tile_order, ws, ws_bytes, (cudaStream_t)stream, counts);
 }

@@ -254,7 +254,8 @@ class Rasterizer:
         # device-count binning (set by the Trainer): an int64[2] step state shared by the
         # views of a step and the instance capacity of this rasteriser's pooled buffers
         self.device_counts: torch.Tensor | None = None
-        self.inst_cap = 0
+        self.inst_cap = 0  # tile instances a view may have
+        self.kept_cap = 0  # kept splats a view may have (sizes the placement's chunk grid)
 
     @staticmethod
     def _placement(width: int, height: int) -> bool:
@@ -333,7 +334,7 @@ class Rasterizer:
             # above the instance capacity is emptied and flagged in the step state
             poison = A.get("poison", 1, torch.int32)
             self._run("vegs_bin_count_dev", _p(tiles), n, _p(offsets), _p(kept_idx), _p(counts),
-                      int(self.inst_cap), _p(self.device_counts), _p(poison), _p(ws),
+                      int(self.inst_cap), int(self.kept_cap), _p(self.device_counts), _p(poison), _p(ws),
                       ctypes.byref(ctypes.c_size_t(wsz)), s)
             return dict(A=A, n=n, record=record, rect=rect, tiles=tiles, depth_key=depth_key, width=width,
                         height=height, background=background, cs=cs, tf=tf, params=params, want_order=want_order,
@@ -369,8 +370,8 @@ class Rasterizer:
             # capacity-sized buffers, counts read by the kernels from the device
             n_kept = n_inst = int(self.inst_cap)
             sorted_gauss = A.get("sorted_gauss", n_inst, torch.int32)
-            args = (_p(depth_key), _p(rect), _p(offsets), _p(kept_idx), n, _p(pend["counts"]), width, height, TILE,
-                    _p(sorted_gauss), _p(tile_start), _p(tile_end), _p(tile_order))
+            args = (_p(depth_key), _p(rect), _p(offsets), _p(kept_idx), n, _p(pend["counts"]), int(self.kept_cap),
+                    width, height, TILE, _p(sorted_gauss), _p(tile_start), _p(tile_end), _p(tile_order))
             wsz = _lib.size_query("vegs_bin_sort_dev", *args, tail=(s,))
             ws = A.get("ws_sort", wsz, torch.uint8)
             self._run("vegs_bin_sort_dev", *args, _p(ws), ctypes.byref(ctypes.c_size_t(wsz)), s)

@@ -237,8 +237,9 @@ class Trainer:
         self._graphs: dict = {}
         self._graph_pool = None
         self._replayed_launches = 0
-        self._state = torch.zeros(2, dtype=torch.int64, device=self.device)  # [overflow, max instances]
-        self._state_host = torch.zeros(2, dtype=torch.int64, pin_memory=True)
+        # [overflow, max instances, max kept splats] of the views of the current step
+        self._state = torch.zeros(3, dtype=torch.int64, device=self.device)
+        self._state_host = torch.zeros(3, dtype=torch.int64, pin_memory=True)
         self._state_event = torch.cuda.Event()
         self.set_graphs(graphs)
 
@@ -248,6 +249,9 @@ class Trainer:
         self.graphs = on
         if on and self._graph_pool is None:
             self._graph_pool = torch.cuda.graph_pool_handle()
+        if on and self.lanes[0].stream == torch.cuda.default_stream(self.device):
+            # the legacy default stream cannot join a captured graph: lane 0 gets its own
+            self.lanes[0].stream = torch.cuda.Stream(self.device)
         for lane in self.lanes:
             lane.rz.device_counts = self._state if on else None
 
@@ -456,8 +460,10 @@ class Trainer:
             # overflow: grow every lane's capacity to the largest view seen, forget the graphs
             # (their buffers are the old size), restore the densify statistics, redo the step
             cap = int(int(self._state_host[1]) * 1.25) + 4096
+            kcap = int(int(self._state_host[2]) * 1.25) + 1024
             for lane in self.lanes:
                 lane.rz.inst_cap = max(lane.rz.inst_cap, cap)
+                lane.rz.kept_cap = max(lane.rz.kept_cap, kcap)
                 if self.densify_stats is not None and lane.dstats is not None:
                     lane.dstats.copy_(lane.dstats_saved)
             self._graphs.clear()
