@@ -644,8 +644,9 @@ def run_c4(args, dev, rank, world) -> dict:
     def views_for(s):
         return view_sets[used[s]]
 
-    for k in sorted(set(used)):  # warm-up: every TF's view set once (and its graph captured)
-        tr.step(view_sets[k], total_views=len(cams))
+    for _ in range(2):  # warm-up: every TF's view set twice (capacities settle, then graphs are captured)
+        for k in sorted(set(used)):
+            tr.step(view_sets[k], total_views=len(cams))
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
@@ -672,7 +673,7 @@ def run_c4(args, dev, rank, world) -> dict:
                         "prune on max TF opacity < 0.005 over the 16 TFs, capped at 3M)",
             "steps_per_s": 1000.0 / step_ms, "ms_per_step": step_ms, "densify_ms": dens_ms,
             "steps_per_s_amortised": 1000.0 / (step_ms + dens_ms / 100.0), "n_before": n_before,
-            "n_after": n_after, "timed_steps": steps}
+            "n_after": n_after, "timed_steps": steps, "graph_stats": dict(tr.graph_stats)}
 
 
 # -- the CPU arm (oracle restatement of the reference algorithm) -------------------------

@@ -237,6 +237,7 @@ class Trainer:
         self._graphs: dict = {}
         self._graph_pool = None
         self._replayed_launches = 0
+        self.graph_stats = {"captures": 0, "replays": 0, "redos": 0}
         # [overflow, max instances, max kept splats] of the views of the current step
         self._state = torch.zeros(3, dtype=torch.int64, device=self.device)
         self._state_host = torch.zeros(3, dtype=torch.int64, pin_memory=True)
@@ -449,6 +450,7 @@ class Trainer:
                 entry[0].replay()
                 loss = entry[1]
                 self._replayed_launches += entry[2]
+                self.graph_stats["replays"] += 1
             else:
                 loss = self._step_body(views, total, self._hyper_dev, self._state)
             self._state_event.record(torch.cuda.current_stream(self.device))
@@ -459,6 +461,7 @@ class Trainer:
                 return loss
             # overflow: grow every lane's capacity to the largest view seen, forget the graphs
             # (their buffers are the old size), restore the densify statistics, redo the step
+            self.graph_stats["redos"] += 1
             cap = int(int(self._state_host[1]) * 1.25) + 4096
             kcap = int(int(self._state_host[2]) * 1.25) + 1024
             for lane in self.lanes:
@@ -481,6 +484,7 @@ class Trainer:
         captured = sum(lane.rz.launches + lane.loss_launches for lane in self.lanes) - before
         self._replayed_launches -= captured  # the capture itself launched nothing; replays count them
         self._graphs[key] = (g, loss, captured)
+        self.graph_stats["captures"] += 1
 
     def track_densify(self, on: bool = True) -> None:
         """Accumulate DensifyStats (per view, fused into the backward) from now on."""
