@@ -456,7 +456,9 @@ class Trainer:
             self._state_event.record(torch.cuda.current_stream(self.device))
             self._state_event.synchronize()
             if not int(self._state_host[0]):
-                if entry is None and uniform and views:
+                # (with a process group the steps stay eager: device counts, no per-view sync,
+                # but the NCCL all-reduce is not captured -- never exercised on one GPU)
+                if entry is None and uniform and views and self.group is None:
                     self._capture(key, views, total)
                 return loss
             # overflow: grow every lane's capacity to the largest view seen, forget the graphs
