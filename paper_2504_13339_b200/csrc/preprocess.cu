@@ -139,7 +139,7 @@ __global__ void __launch_bounds__(256) adam_kernel(double *params, GradParts gp,
     const int cls = kUnitClass[unit];
     const double b1 = 0.9, b2 = 0.999, eps = 1e-15;
     const double lr_c = params ? lr[cls] : 0.0;
-    if (bias1 != bias1) {  // NaN marks "from the device": lr[10], lr[11] hold 1 - beta^t (graph replay)
+    if (params && bias1 != bias1) {  // NaN marks "from the device": lr[10], lr[11] hold 1 - beta^t (graph replay)
         bias1 = lr[10];
         bias2 = lr[11];
     }
