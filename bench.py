@@ -169,7 +169,7 @@ class KernelTimer:
             if recs:
                 ms = [a.elapsed_time(b) for a, b, _ in recs]
                 out[name] = dict(launches=len(recs), avg_ms=sum(ms) / len(ms), total_ms=sum(ms),
-                                 counts=[c for _, _, c in recs])
+                                 counts=[c for _, _, c in recs], events=recs)
         return out
 
 
@@ -219,7 +219,16 @@ def composite_roofline(ksum: dict, pixels: int, ncu_key: str, ncu_file: str = "n
     if prof.exists():
         r = json.loads(prof.read_text()).get(ncu_key)
         if r:
-            scale = out["avg_instances"] / r["instances"] if r.get("instances") else 1.0
+            ms_issue = rec["avg_ms"]
+            scale = 1.0
+            if r.get("instances"):
+                # the launches of the very frame the capture profiled (same instance count):
+                # their own live duration against the capture's instruction count
+                same = [(a.elapsed_time(b)) for (a, b, c) in rec.get("events", []) if c[1] == int(r["instances"])]
+                if same:
+                    ms_issue = sum(same) / len(same)
+                else:
+                    scale = out["avg_instances"] / r["instances"]
             out["traffic"] = r["dram_bytes"] * scale
             mhz = MAX_SM_MHZ
             try:
@@ -229,12 +238,14 @@ def composite_roofline(ksum: dict, pixels: int, ncu_key: str, ncu_file: str = "n
             sms = torch.cuda.get_device_properties(torch.cuda.current_device()).multi_processor_count
             peak_issue = sms * 4 * mhz * 1e6
             wi = r["warp_instructions"] * scale
-            out["issue_roofline"] = {"bound": "issue", "achieved": wi / (rec["avg_ms"] / 1000.0), "peak": peak_issue,
+            out["issue_roofline"] = {"bound": "issue", "achieved": wi / (ms_issue / 1000.0), "peak": peak_issue,
                                      "unit": "warp-instructions/s",
-                                     "frac": wi / (rec["avg_ms"] / 1000.0) / peak_issue,
-                                     "warp_instructions_per_launch": wi,
+                                     "frac": wi / (ms_issue / 1000.0) / peak_issue,
+                                     "warp_instructions_per_launch": wi, "launch_ms": ms_issue,
                                      "source": f"profiles/{ncu_file}[{ncu_key}]"
-                                               + (" scaled by live/profiled instances" if scale != 1.0 else "")}
+                                               + (" scaled by live/profiled instances" if scale != 1.0 else
+                                                  (" over the live launches of the profiled frame"
+                                                   if r.get("instances") else ""))}
     return out
 
 
