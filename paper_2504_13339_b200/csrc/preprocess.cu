@@ -235,9 +235,11 @@ static int adam_launch(double *params, GradParts gp, double *m, double *v, int64
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    int bx = (int)((n + 255) / 256);
-    const int cap = (sms * 8 + 18) / 19;  // ~8 resident 256-thread CTAs per SM over the 19 units
-    if (bx > cap) bx = cap;
+    // one element per thread: every load of the step (4 gradient partials, params, m, v) in
+    // flight at once across the grid (the grid-stride version capped at 8 CTAs per SM was
+    // load-latency bound: 55% long-scoreboard stalls, 42% of HBM)
+    const int bx = (int)((n + 255) / 256);
+    (void)sms;
     adam_kernel<<<dim3(bx, 19), 256, 0, (cudaStream_t)stream>>>(params, gp, m, v, n, lr, grad_scale, bias1, bias2,
                                                                 nonfinite, skip);
     VEGS_CHECK_LAUNCH();
