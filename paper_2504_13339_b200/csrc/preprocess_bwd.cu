@@ -26,15 +26,36 @@ namespace vegs {
 // (L2-resident, one bit per instance) means only the ~30% of rows a pixel actually
 // blended are read.  The register-heavy chain runs separately.
 
-template <typename Real, int NV>
 #ifndef VEGS_RR_T
 #define VEGS_RR_T 64  // small CTAs: the per-Gaussian walks are uneven (3.5 active lanes per warp)
 #endif
+template <typename Real, int NV>
+__device__ __forceinline__ void reduce_rows_one(const uint32_t *tiles, const int64_t *offsets, const Real *rows,
+                                                const uint32_t *visited, double *sums, int64_t g);
+
+template <typename Real, int NV>
 __global__ void __launch_bounds__(VEGS_RR_T) reduce_rows_kernel(const uint32_t *tiles, const int64_t *offsets,
                                                           const Real *rows, int64_t n, const uint32_t *visited,
                                                           double *sums) {
     const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (g >= n) return;
+    reduce_rows_one<Real, NV>(tiles, offsets, rows, visited, sums, g);
+}
+
+// the same over a compacted list of the kept Gaussians (count on the device)
+template <typename Real, int NV>
+__global__ void __launch_bounds__(VEGS_RR_T) reduce_rows_list_kernel(const uint32_t *tiles, const int64_t *offsets,
+                                                               const Real *rows, const int32_t *list,
+                                                               const int32_t *count, const uint32_t *visited,
+                                                               double *sums) {
+    const int m = *count;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < m; i += gridDim.x * blockDim.x)
+        reduce_rows_one<Real, NV>(tiles, offsets, rows, visited, sums, list[i]);
+}
+
+template <typename Real, int NV>
+__device__ __forceinline__ void reduce_rows_one(const uint32_t *tiles, const int64_t *offsets, const Real *rows,
+                                                const uint32_t *visited, double *sums, int64_t g) {
     const uint32_t cnt = tiles[g];
     if (cnt == 0) return;
     constexpr int RS = ((7 + (NV - 6)) + 3) & ~3;
@@ -278,6 +299,32 @@ __global__ void __launch_bounds__(VEGS_PBWD_T, VEGS_PBWD_MINB) preprocess_bwd_ke
 // camera-space position), the shininess clamp gate, and the sign of n.l when it is within
 // float32 rounding of zero.  Decisions identical, arithmetic ~1e-6 relative: far inside the
 // 1e-4 gradient bar (tests hold the results to the reference at 1e-4).
+// Kept Gaussians appended to a list (warp-aggregated, order irrelevant: every Gaussian's
+// outputs depend on it alone); the others get their zero outputs here, so the float32
+// chain and its row reduction run only over the kept splats (config 4: 8k of 200k).
+__global__ void __launch_bounds__(256) kept_list_kernel(const uint32_t *tiles, int64_t n, int accumulate,
+                                                        double *grads, double *vs_norm, uint8_t *visible_out,
+                                                        int32_t *list, int32_t *count) {
+    const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const bool in = g < n;
+    const bool kept = in && tiles[g] != 0u;
+    const unsigned bal = __ballot_sync(0xffffffffu, kept);
+    const int lane = threadIdx.x & 31;
+    int base = 0;
+    if (lane == 0 && bal) base = atomicAdd(count, __popc(bal));
+    base = __shfl_sync(0xffffffffu, base, 0);
+    if (kept) list[base + __popc(bal & ((1u << lane) - 1u))] = (int32_t)g;
+    if (!in || kept) return;
+    if (!accumulate) {
+        GradView G(grads, n);
+        for (int k = 0; k < 3; ++k) G.pos[3 * g + k] = 0.0, G.log_scale[3 * g + k] = 0.0, G.normal[3 * g + k] = 0.0;
+        for (int k = 0; k < 4; ++k) G.rot[4 * g + k] = 0.0;
+        G.raw_value[g] = G.raw_weight[g] = G.raw_ka[g] = G.raw_kd[g] = G.raw_ks[g] = G.raw_beta[g] = 0.0;
+    }
+    if (vs_norm) vs_norm[g] = 0.0;
+    if (visible_out) visible_out[g] = 0;
+}
+
 #ifndef VEGS_PBWD32_MINB
 #define VEGS_PBWD32_MINB 3  // 80 registers: 3 x 256 threads per SM (2: 0.344 ms, 4: 0.378 ms per c2 view, both worse)
 #endif
@@ -296,28 +343,32 @@ __device__ __noinline__ float ndotl_sign_f64(const ParamView &P, int64_t g, cons
 }
 
 template <int n_ch>
+__device__ __forceinline__ void preprocess_bwd32_one(const double *params, int64_t n, const VegsCamera &cam,
+                                                     const TFTable &tab, const VegsSettings &st, const double *sums,
+                                                     double scale, int accumulate, double *grads, double *vs_norm,
+                                                     uint8_t *visible_out, double *dstats, int64_t g);
+
+// over the compacted list of kept Gaussians (kept_list_kernel), a persistent grid: the TF
+// table is staged once per CTA instead of once per 256 Gaussians
+template <int n_ch>
 __global__ void __launch_bounds__(VEGS_PBWD_T, VEGS_PBWD32_MINB) preprocess_bwd32_kernel(
-    const double *params, int64_t n, VegsCamera cam, VegsTF tf, VegsSettings st,
-    const uint32_t *tiles, const double *sums, double scale, int accumulate,
-    double *grads, double *vs_norm, uint8_t *visible_out, double *dstats) {
+    const double *params, int64_t n, VegsCamera cam, VegsTF tf, VegsSettings st, const int32_t *list,
+    const int32_t *count, const double *sums, double scale, int accumulate, double *grads, double *vs_norm,
+    uint8_t *visible_out, double *dstats) {
     extern __shared__ double tf_smem[];
     const TFTable tab = stage_tf(tf, tf_smem);
-    const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (g >= n) return;
+    const int m = *count;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < m; i += gridDim.x * blockDim.x)
+        preprocess_bwd32_one<n_ch>(params, n, cam, tab, st, sums, scale, accumulate, grads, vs_norm, visible_out,
+                                   dstats, list[i]);
+}
+
+template <int n_ch>
+__device__ __forceinline__ void preprocess_bwd32_one(const double *params, int64_t n, const VegsCamera &cam,
+                                                     const TFTable &tab, const VegsSettings &st, const double *sums,
+                                                     double scale, int accumulate, double *grads, double *vs_norm,
+                                                     uint8_t *visible_out, double *dstats, int64_t g) {
     GradView G(grads, n);
-    const uint32_t cnt = tiles[g];
-    if (cnt == 0) {
-        if (!accumulate) {
-            for (int k = 0; k < 3; ++k) G.pos[3 * g + k] = 0.0, G.log_scale[3 * g + k] = 0.0,
-                                         G.normal[3 * g + k] = 0.0;
-            for (int k = 0; k < 4; ++k) G.rot[4 * g + k] = 0.0;
-            G.raw_value[g] = G.raw_weight[g] = G.raw_ka[g] = G.raw_kd[g] = G.raw_ks[g] =
-                G.raw_beta[g] = 0.0;
-        }
-        if (vs_norm) vs_norm[g] = 0.0;
-        if (visible_out) visible_out[g] = 0;
-        return;
-    }
     // every input of this Gaussian loaded up front (independent loads in flight together;
     // the outputs are written in one batch at the end)
     const double *red = sums + (int64_t)row_width(n_ch) * g;
@@ -583,7 +634,8 @@ extern "C" int vegs_preprocess_backward(const double *params, int64_t n, const V
                                         double *densify_stats, const uint32_t *inst_visited, void *ws, size_t *ws_bytes,
                                         void *stream) {
     if (!ws_bytes || (n_channels != 3 && n_channels != 11)) return VEGS_ERR_ARG;
-    const size_t need = sizeof(double) * (size_t)row_width(n_channels) * (size_t)(n > 0 ? n : 1);
+    const size_t sums_bytes = (sizeof(double) * (size_t)row_width(n_channels) * (size_t)(n > 0 ? n : 1) + 255) & ~size_t(255);
+    const size_t need = sums_bytes + sizeof(int32_t) * (size_t)(n + 64);  // + the kept list and its count
     if (!ws) {
         *ws_bytes = need;
         return VEGS_OK;
@@ -595,6 +647,44 @@ extern "C" int vegs_preprocess_backward(const double *params, int64_t n, const V
     const int rr_blocks = (int)((n + VEGS_RR_T - 1) / VEGS_RR_T);
     cudaStream_t s = (cudaStream_t)stream;
     double *sums = (double *)ws;
+    const char *chain64 = getenv("VEGS_BWD_CHAIN_F64");  // test switch: float64 chain for float32 blends
+    if (!store_f64 && !(chain64 && chain64[0] && chain64[0] != '0')) {
+        // float32 blends: the kept Gaussians compacted once, the row sums and the float32
+        // chain over that list only
+        int32_t *count = reinterpret_cast<int32_t *>(reinterpret_cast<char *>(ws) + sums_bytes);
+        int32_t *list = count + 64;
+        int dev = 0, sms = 148;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        VEGS_CUDA(cudaMemsetAsync(count, 0, sizeof(int32_t), s));
+        kept_list_kernel<<<(int)((n + 255) / 256), 256, 0, s>>>(tiles, n, accumulate, grads, viewspace_norm, visible,
+                                                                 list, count);
+        VEGS_CHECK_LAUNCH();
+        const int rr_list_blocks = rr_blocks < sms * 32 ? rr_blocks : sms * 32;
+        if (n_channels == 3)
+            reduce_rows_list_kernel<float, 9><<<rr_list_blocks, VEGS_RR_T, 0, s>>>(tiles, offsets, (const float *)inst_rows,
+                                                                               list, count, inst_visited, sums);
+        else
+            reduce_rows_list_kernel<float, 17><<<rr_list_blocks, VEGS_RR_T, 0, s>>>(tiles, offsets, (const float *)inst_rows,
+                                                                                list, count, inst_visited, sums);
+        VEGS_CHECK_LAUNCH();
+        const size_t smem = tf_smem_bytes(*tf);
+        const int full = (int)((n + VEGS_PBWD_T - 1) / VEGS_PBWD_T);
+        const int blocks = full < sms * VEGS_PBWD32_MINB ? full : sms * VEGS_PBWD32_MINB;
+        if (n_channels == 3) {
+            VEGS_CUDA(cudaFuncSetAttribute(preprocess_bwd32_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            preprocess_bwd32_kernel<3><<<blocks, VEGS_PBWD_T, smem, s>>>(params, n, *cam, *tf, *st, list, count, sums,
+                                                                         scale, accumulate, grads, viewspace_norm,
+                                                                         visible, densify_stats);
+        } else {
+            VEGS_CUDA(cudaFuncSetAttribute(preprocess_bwd32_kernel<11>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            preprocess_bwd32_kernel<11><<<blocks, VEGS_PBWD_T, smem, s>>>(params, n, *cam, *tf, *st, list, count, sums,
+                                                                          scale, accumulate, grads, viewspace_norm,
+                                                                          visible, densify_stats);
+        }
+        VEGS_CHECK_LAUNCH();
+        return VEGS_OK;
+    }
     if (store_f64) {
         if (n_channels == 3) reduce_rows_kernel<double, 9><<<rr_blocks, VEGS_RR_T, 0, s>>>(tiles, offsets, (const double *)inst_rows, n, inst_visited, sums);
         else reduce_rows_kernel<double, 17><<<rr_blocks, VEGS_RR_T, 0, s>>>(tiles, offsets, (const double *)inst_rows, n, inst_visited, sums);
@@ -604,23 +694,6 @@ extern "C" int vegs_preprocess_backward(const double *params, int64_t n, const V
     }
     VEGS_CHECK_LAUNCH();
     const size_t smem = tf_smem_bytes(*tf);
-    const char *chain64 = getenv("VEGS_BWD_CHAIN_F64");  // test switch: float64 chain for float32 blends
-    if (!store_f64 && !(chain64 && chain64[0] && chain64[0] != '0')) {
-        const int blocks = (int)((n + VEGS_PBWD_T - 1) / VEGS_PBWD_T);
-        if (n_channels == 3) {
-            VEGS_CUDA(cudaFuncSetAttribute(preprocess_bwd32_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-            preprocess_bwd32_kernel<3><<<blocks, VEGS_PBWD_T, smem, s>>>(params, n, *cam, *tf, *st, tiles, sums, scale,
-                                                                         accumulate, grads, viewspace_norm, visible,
-                                                                         densify_stats);
-        } else {
-            VEGS_CUDA(cudaFuncSetAttribute(preprocess_bwd32_kernel<11>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-            preprocess_bwd32_kernel<11><<<blocks, VEGS_PBWD_T, smem, s>>>(params, n, *cam, *tf, *st, tiles, sums, scale,
-                                                                          accumulate, grads, viewspace_norm, visible,
-                                                                          densify_stats);
-        }
-        VEGS_CHECK_LAUNCH();
-        return VEGS_OK;
-    }
     VEGS_CUDA(cudaFuncSetAttribute(preprocess_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     preprocess_bwd_kernel<<<(int)((n + VEGS_PBWD_T - 1) / VEGS_PBWD_T), VEGS_PBWD_T, smem, s>>>(params, n, *cam, *tf, *st, n_channels, tiles, sums, scale,
                                                     accumulate, grads, viewspace_norm, visible, densify_stats);

@@ -47,7 +47,7 @@ LAUNCHES = {
     "vegs_composite_forward": 1,
     "vegs_composite_forward_fast": 2,  # blend + float64 fix-up of the undecidable pixels (+ a 4-byte memset)
     "vegs_composite_backward": 1,
-    "vegs_preprocess_backward": 2,  # row reduction + chain
+    "vegs_preprocess_backward": 3,  # kept list + row reduction + chain (float32 blends; float64: 2)
     "vegs_loss_l1_ssim": 2,
     "vegs_loss_aux": 3,
     "vegs_adam_step": 1,
