@@ -24,6 +24,11 @@ namespace vegs {
 #endif
 constexpr int kWin = 11, kHalf = 5, kLT = VEGS_SSIM_TILE;  // window, half window, output tile
 constexpr int kIn = kLT + kWin - 1;                         // staged input tile side
+#ifndef VEGS_SSIM_RB
+#define VEGS_SSIM_RB 4
+#endif
+constexpr int kRB = VEGS_SSIM_RB;  // outputs per thread in each blur pass (register blocking)
+static_assert(kLT % kRB == 0, "register blocks tile the output");
 
 struct Taps {
     float k[kWin];
@@ -63,25 +68,49 @@ __global__ void __launch_bounds__(VEGS_SSIM_T) ssim_fwd_kernel(const float *__re
                            : make_float2(0.f, 0.f);
         }
         __syncthreads();
-        for (int i = threadIdx.x; i < kIn * kLT; i += blockDim.x) {
-            const int r = i / kLT, q = i - r * kLT;
-            float2 m01 = make_float2(0.f, 0.f), m23 = make_float2(0.f, 0.f);
-            float m4 = 0.f;
+        // horizontal pass, register-blocked: one thread, kRB consecutive outputs of a row,
+        // each staged value (and its squares / cross product) loaded and formed once
+        for (int i = threadIdx.x; i < kIn * (kLT / kRB); i += blockDim.x) {
+            const int r = i / (kLT / kRB), q0 = (i - r * (kLT / kRB)) * kRB;
+            float2 v[kWin + kRB - 1], sq[kWin + kRB - 1];
+            float pr[kWin + kRB - 1];
 #pragma unroll
-            for (int t = 0; t < kWin; ++t) {
-                const float2 v = sxy[r][q + t];
-                const float2 k = make_float2(taps.k[t], taps.k[t]);
-                m01 = __ffma2_rn(k, v, m01);
-                m23 = __ffma2_rn(k, __fmul2_rn(v, v), m23);
-                m4 += taps.k[t] * (v.x * v.y);
+            for (int t = 0; t < kWin + kRB - 1; ++t) {
+                v[t] = sxy[r][q0 + t];
+                sq[t] = __fmul2_rn(v[t], v[t]);
+                pr[t] = v[t].x * v[t].y;
             }
-            h01[r][q] = m01;
-            h23[r][q] = m23;
-            h4[r][q] = m4;
+#pragma unroll
+            for (int o = 0; o < kRB; ++o) {
+                float2 m01 = make_float2(0.f, 0.f), m23 = make_float2(0.f, 0.f);
+                float m4 = 0.f;
+#pragma unroll
+                for (int t = 0; t < kWin; ++t) {
+                    const float2 k = make_float2(taps.k[t], taps.k[t]);
+                    m01 = __ffma2_rn(k, v[o + t], m01);
+                    m23 = __ffma2_rn(k, sq[o + t], m23);
+                    m4 += taps.k[t] * pr[o + t];
+                }
+                h01[r][q0 + o] = m01;
+                h23[r][q0 + o] = m23;
+                h4[r][q0 + o] = m4;
+            }
         }
         __syncthreads();
-        for (int i = threadIdx.x; i < kLT * kLT; i += blockDim.x) {
-            const int r = i / kLT, q = i - r * kLT;
+        // vertical pass, register-blocked: one thread, kRB consecutive rows of a column
+        for (int i = threadIdx.x; i < (kLT / kRB) * kLT; i += blockDim.x) {
+            const int r0 = (i / kLT) * kRB, q = i - (i / kLT) * kLT;
+            float2 a01[kWin + kRB - 1], a23[kWin + kRB - 1];
+            float a4[kWin + kRB - 1];
+#pragma unroll
+            for (int t = 0; t < kWin + kRB - 1; ++t) {
+                a01[t] = h01[r0 + t][q];
+                a23[t] = h23[r0 + t][q];
+                a4[t] = h4[r0 + t][q];
+            }
+#pragma unroll
+            for (int o = 0; o < kRB; ++o) {
+            const int r = r0 + o;
             const int u = u0 + r, v = v0 + q;
             if (u >= Hv || v >= Wv) continue;
             float2 m01 = make_float2(0.f, 0.f), m23 = make_float2(0.f, 0.f);
@@ -89,9 +118,9 @@ __global__ void __launch_bounds__(VEGS_SSIM_T) ssim_fwd_kernel(const float *__re
 #pragma unroll
             for (int t = 0; t < kWin; ++t) {
                 const float2 k = make_float2(taps.k[t], taps.k[t]);
-                m01 = __ffma2_rn(k, h01[r + t][q], m01);
-                m23 = __ffma2_rn(k, h23[r + t][q], m23);
-                m4 += taps.k[t] * h4[r + t][q];
+                m01 = __ffma2_rn(k, a01[o + t], m01);
+                m23 = __ffma2_rn(k, a23[o + t], m23);
+                m4 += taps.k[t] * a4[o + t];
             }
             const float mux = m01.x, muy = m01.y;
             const float sxx = m23.x - mux * mux, syy = m23.y - muy * muy, sxy_ = m4 - mux * muy;
@@ -104,10 +133,11 @@ __global__ void __launch_bounds__(VEGS_SSIM_T) ssim_fwd_kernel(const float *__re
                                         2.f * mux * smap / b2);
             const float g_xx = coeff * (-smap / b2);
             const float g_xy = coeff * (2.f * a1 * inv);
-            const int64_t o = (int64_t)c * plane + (int64_t)u * Wv + v;
-            maps[o] = g_mu;
-            maps[3 * plane + o] = g_xx;
-            maps[6 * plane + o] = g_xy;
+            const int64_t oo = (int64_t)c * plane + (int64_t)u * Wv + v;
+            maps[oo] = g_mu;
+            maps[3 * plane + oo] = g_xx;
+            maps[6 * plane + oo] = g_xy;
+            }
         }
     }
     const float tot = block_sum_f(local, red);
@@ -138,22 +168,42 @@ __global__ void __launch_bounds__(VEGS_SSIM_T) ssim_bwd_kernel(const float *__re
             sm2[r][q] = ok ? maps[6 * plane + o] : 0.f;
         }
         __syncthreads();
-        for (int i = threadIdx.x; i < kIn * kLT; i += blockDim.x) {
-            const int r = i / kLT, q = i - r * kLT;
-            float2 a01 = make_float2(0.f, 0.f);
-            float a2 = 0.f;
+        for (int i = threadIdx.x; i < kIn * (kLT / kRB); i += blockDim.x) {  // register-blocked, as in the forward
+            const int r = i / (kLT / kRB), q0 = (i - r * (kLT / kRB)) * kRB;
+            float2 w01[kWin + kRB - 1];
+            float w2[kWin + kRB - 1];
 #pragma unroll
-            for (int t = 0; t < kWin; ++t) {
-                const float k = taps.k[kWin - 1 - t];
-                a01 = __ffma2_rn(make_float2(k, k), sm01[r][q + t], a01);
-                a2 += k * sm2[r][q + t];
+            for (int t = 0; t < kWin + kRB - 1; ++t) {
+                w01[t] = sm01[r][q0 + t];
+                w2[t] = sm2[r][q0 + t];
             }
-            hs01[r][q] = a01;
-            hs2[r][q] = a2;
+#pragma unroll
+            for (int o = 0; o < kRB; ++o) {
+                float2 a01 = make_float2(0.f, 0.f);
+                float a2 = 0.f;
+#pragma unroll
+                for (int t = 0; t < kWin; ++t) {
+                    const float k = taps.k[kWin - 1 - t];
+                    a01 = __ffma2_rn(make_float2(k, k), w01[o + t], a01);
+                    a2 += k * w2[o + t];
+                }
+                hs01[r][q0 + o] = a01;
+                hs2[r][q0 + o] = a2;
+            }
         }
         __syncthreads();
-        for (int i = threadIdx.x; i < kLT * kLT; i += blockDim.x) {
-            const int r = i / kLT, q = i - r * kLT;
+        for (int i = threadIdx.x; i < (kLT / kRB) * kLT; i += blockDim.x) {
+            const int r0 = (i / kLT) * kRB, q = i - (i / kLT) * kLT;
+            float2 w01[kWin + kRB - 1];
+            float w2[kWin + kRB - 1];
+#pragma unroll
+            for (int t = 0; t < kWin + kRB - 1; ++t) {
+                w01[t] = hs01[r0 + t][q];
+                w2[t] = hs2[r0 + t][q];
+            }
+#pragma unroll
+            for (int o = 0; o < kRB; ++o) {
+            const int r = r0 + o;
             const int gi = i0 + r, gj = j0 + q;
             if (gi >= H || gj >= W) continue;
             float2 a01 = make_float2(0.f, 0.f);
@@ -161,8 +211,8 @@ __global__ void __launch_bounds__(VEGS_SSIM_T) ssim_bwd_kernel(const float *__re
 #pragma unroll
             for (int t = 0; t < kWin; ++t) {
                 const float k = taps.k[kWin - 1 - t];
-                a01 = __ffma2_rn(make_float2(k, k), hs01[r + t][q], a01);
-                a2 += k * hs2[r + t][q];
+                a01 = __ffma2_rn(make_float2(k, k), w01[o + t], a01);
+                a2 += k * w2[o + t];
             }
             const float acc[3] = {a01.x, a01.y, a2};
             const int64_t pix = (int64_t)gi * W + gj;
@@ -172,6 +222,7 @@ __global__ void __launch_bounds__(VEGS_SSIM_T) ssim_bwd_kernel(const float *__re
             l1 += fabsf(d);
             const float sgn = d > 0.f ? 1.f : (d < 0.f ? -1.f : 0.f);
             dx[p] = l1_coeff * sgn + acc[0] + 2.f * xv * acc[1] + yv * acc[2];
+            }
         }
     }
     const float tot = block_sum_f(l1, red);
