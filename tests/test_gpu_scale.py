@@ -546,3 +546,15 @@ def test_graph_step_overflow_regrows_and_redoes():
     res = _graph_runs(lambda s: views if s < 2 else views2, 4)
     assert res[False][0] == res[True][0]
     assert torch.equal(res[False][1], res[True][1])
+
+
+@pytest.mark.parametrize("lanes,aux", [(1, False), (2, True)])
+def test_graph_steps_other_lane_counts_and_aux(lanes, aux):
+    """Graph-replayed steps with one lane (no look-ahead) and with the 11-plane aux loss:
+    bitwise the eager steps."""
+    learned, dtf, cams, targets = _train_scene(3)
+    views = [View(c, dtf, t) for c, t in zip(cams, targets)]
+    res = _graph_runs(lambda s: views, 3, lanes=lanes, with_aux=aux)
+    assert res[False][0] == res[True][0]
+    assert torch.equal(res[False][1], res[True][1])
+    assert res[True][3].graph_stats["replays"] >= 1
