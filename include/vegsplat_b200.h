@@ -213,19 +213,21 @@ int vegs_composite_backward(const int32_t *tile_start, const int32_t *tile_end,
                             uint32_t *inst_visited, int64_t n_inst, const int32_t *tile_order,
                             void *stream);
 
-/* Per-Gaussian: float64 reduction of its instance rows (duplicate order == np.add.at
- * order), then projection and shading backward.  grads: flat float64 class-major
- * buffer (19 n); grads = accumulate ? grads + scale * g : scale * g.  viewspace_norm /
- * visible may be NULL.  Only rows whose inst_visited bit is set are summed.  densify_stats (n x 5,
- * may be NULL) accumulates DensifyStats for the kept splats.  ws holds the per-Gaussian
- * sums (n x (6 + C) float64). */
+/* Per-Gaussian: reduction of its instance rows (duplicate order == np.add.at order;
+ * float64 rows in float64, float32 rows in float32), then projection and shading
+ * backward.  grads: flat float64 class-major buffer (19 n); grads = accumulate ? grads +
+ * scale * g : scale * g.  viewspace_norm / visible may be NULL.  Only rows whose
+ * inst_visited bit is set are summed.  densify_stats (n x 5, may be NULL) accumulates
+ * DensifyStats for the kept splats.  kept_bound: an upper bound on the kept splats (<= 0:
+ * n) that sizes the float32 path's grids over its compacted kept list.  ws holds the
+ * per-Gaussian sums (n x (6 + C) float64) and the kept list. */
 int vegs_preprocess_backward(const double *params, int64_t n, const VegsCamera *cam,
                              const VegsTF *tf, const VegsSettings *st, int32_t n_channels,
                              int32_t store_f64, const uint32_t *tiles, const int64_t *offsets,
                              const void *inst_rows, double scale, int32_t accumulate,
                              double *grads, double *viewspace_norm, uint8_t *visible,
-                             double *densify_stats, const uint32_t *inst_visited, void *ws,
-                             size_t *ws_bytes, void *stream);
+                             double *densify_stats, const uint32_t *inst_visited, int64_t kept_bound,
+                             void *ws, size_t *ws_bytes, void *stream);
 
 /* ---- drop-in raw kernels (reference argument lists) -------------------------------- */
 int vegs_blend_forward(const int64_t *tile_start, const int64_t *tile_end, int64_t n_tiles,

@@ -64,7 +64,7 @@ _SIGS = {
     "vegs_composite_backward": [P, P, P, P, P, P, c_int32, c_int32, P, c_int32, c_int32, c_double, P, P,
                                 P, P, P, P, c_int64, P, P],
     "vegs_preprocess_backward": [P, c_int64, POINTER(VegsCamera), POINTER(VegsTF), POINTER(VegsSettings),
-                                 c_int32, c_int32, P, P, P, c_double, c_int32, P, P, P, P, P, P,
+                                 c_int32, c_int32, P, P, P, c_double, c_int32, P, P, P, P, P, c_int64, P,
                                  POINTER(c_size_t), P],
     "vegs_densify_count": [P, c_int64, P, POINTER(VegsDensify), P, P, P, POINTER(c_size_t), P],
     "vegs_tf_max_opacity": [P, c_int64, POINTER(VegsTF), c_int32, P, P],

@@ -631,8 +631,8 @@ extern "C" int vegs_preprocess_backward(const double *params, int64_t n, const V
                                         int32_t store_f64, const uint32_t *tiles, const int64_t *offsets,
                                         const void *inst_rows, double scale, int32_t accumulate,
                                         double *grads, double *viewspace_norm, uint8_t *visible,
-                                        double *densify_stats, const uint32_t *inst_visited, void *ws, size_t *ws_bytes,
-                                        void *stream) {
+                                        double *densify_stats, const uint32_t *inst_visited, int64_t kept_bound,
+                                        void *ws, size_t *ws_bytes, void *stream) {
     if (!ws_bytes || (n_channels != 3 && n_channels != 11)) return VEGS_ERR_ARG;
     const size_t sums_bytes = (sizeof(double) * (size_t)row_width(n_channels) * (size_t)(n > 0 ? n : 1) + 255) & ~size_t(255);
     const size_t need = sums_bytes + sizeof(int32_t) * (size_t)(n + 64);  // + the kept list and its count
@@ -660,7 +660,9 @@ extern "C" int vegs_preprocess_backward(const double *params, int64_t n, const V
         kept_list_kernel<<<(int)((n + 255) / 256), 256, 0, s>>>(tiles, n, accumulate, grads, viewspace_norm, visible,
                                                                  list, count);
         VEGS_CHECK_LAUNCH();
-        const int rr_list_blocks = rr_blocks < sms * 32 ? rr_blocks : sms * 32;
+        const int64_t kb = kept_bound > 0 && kept_bound < n ? kept_bound : n;
+        const int kb_blocks = (int)((kb + VEGS_RR_T - 1) / VEGS_RR_T);
+        const int rr_list_blocks = kb_blocks < sms * 32 ? kb_blocks : sms * 32;
         if (n_channels == 3)
             reduce_rows_list_kernel<float, 9><<<rr_list_blocks, VEGS_RR_T, 0, s>>>(tiles, offsets, (const float *)inst_rows,
                                                                                list, count, inst_visited, sums);
@@ -669,7 +671,7 @@ extern "C" int vegs_preprocess_backward(const double *params, int64_t n, const V
                                                                                 list, count, inst_visited, sums);
         VEGS_CHECK_LAUNCH();
         const size_t smem = tf_smem_bytes(*tf);
-        const int full = (int)((n + VEGS_PBWD_T - 1) / VEGS_PBWD_T);
+        const int full = (int)((kb + VEGS_PBWD_T - 1) / VEGS_PBWD_T);
         const int blocks = full < sms * VEGS_PBWD32_MINB ? full : sms * VEGS_PBWD32_MINB;
         if (n_channels == 3) {
             VEGS_CUDA(cudaFuncSetAttribute(preprocess_bwd32_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));

@@ -368,7 +368,7 @@ class Rasterizer:
         inst_pid = order = None
         if pend.get("device"):
             # capacity-sized buffers, counts read by the kernels from the device
-            n_kept = n_inst = int(self.inst_cap)
+            n_kept, n_inst = int(self.kept_cap), int(self.inst_cap)  # capacities (the counts stay on the device)
             sorted_gauss = A.get("sorted_gauss", n_inst, torch.int32)
             args = (_p(depth_key), _p(rect), _p(offsets), _p(kept_idx), n, _p(pend["counts"]), int(self.kept_cap),
                     width, height, TILE, _p(sorted_gauss), _p(tile_start), _p(tile_end), _p(tile_order))
@@ -448,7 +448,7 @@ class Rasterizer:
             grads = torch.empty(19 * fr.n, dtype=torch.float64, device=self.device)
         args = (_p(fr.params), fr.n, ctypes.byref(fr.cam), ctypes.byref(fr.tf.struct), ctypes.byref(fr.settings),
                 fr.n_ch, int(fr.store_f64), _p(fr.tiles), _p(fr.offsets), _p(rows), float(scale), int(accumulate),
-                _p(grads), _p(viewspace_norm), _p(visible), _p(densify_stats), _p(fr.visited))
+                _p(grads), _p(viewspace_norm), _p(visible), _p(densify_stats), _p(fr.visited), int(fr.n_kept))
         wsz = _lib.size_query("vegs_preprocess_backward", *args, tail=(_stream(),))
         ws = self._alloc().get("ws_pbwd", wsz, torch.uint8)
         self._run("vegs_preprocess_backward", *args, _p(ws), ctypes.byref(ctypes.c_size_t(wsz)), _stream())
