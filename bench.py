@@ -72,10 +72,15 @@ def parse():
                     help="host-counted eager steps instead of device-count steps replayed as CUDA graphs")
     ap.add_argument("--backend", choices=("nccl", "gloo"), default="nccl",
                     help="gradient all-reduce backend for N>1 (gloo: host-side plumbing check only)")
+    ap.add_argument("--grad-payload", choices=("f32", "f64"), default="f32",
+                    help="N>1: all-reduce payload of the step gradient (Adam stays float64, replicated)")
+    ap.add_argument("--grad-buckets", type=int, default=4,
+                    help="N>1: buckets of the pipelined pack / all-reduce / Adam exchange")
     return ap.parse_args()
 
 
-def config_block(world: int, backend: str = "nccl", graphs: bool | None = True) -> dict:
+def config_block(world: int, backend: str = "nccl", graphs: bool | None = True, payload: str = "f32",
+                 buckets: int = 4) -> dict:
     cfg = {"workload": "c2: 1M Gaussians (seed 0) fit to renders of a 1M-Gaussian 64-blob set (seed 1); "
                         "16 views/step at 1024x1024, 256-knot TF; step = render + L1/SSIM + backward "
                         "+ all-reduce + Adam",
@@ -83,6 +88,9 @@ def config_block(world: int, backend: str = "nccl", graphs: bool | None = True) 
             "loss": "0.8*L1 + 0.2*(1-SSIM) (reference (1-lambda) weighting)",
             "parallelism": f"view-sharded dp{world}" + ("" if world == 1 or backend == "nccl" else f" ({backend})"),
             "l2": "inputs larger than L2 (no flush needed)"}
+    if world > 1:
+        cfg["grad_exchange"] = (f"{buckets} buckets, {payload} payload all-reduce pipelined with the lane sum and "
+                                "Adam per bucket")
     if graphs is not None:
         cfg["step_execution"] = ("device-side instance counts, each step one replayed CUDA graph (all views, lanes, "
                                  "Adam); one host wait per step" if graphs else "eager, one host count read per view")
@@ -291,7 +299,7 @@ def run_b200(args) -> None:
 
     group = dist.group.WORLD if world > 1 else None
     trainer = Trainer(learned, TrainConfig(iterations=30000), group=group, lanes=args.lanes,
-                      graphs=not args.no_graphs)
+                      graphs=not args.no_graphs, grad_payload=args.grad_payload, grad_buckets=args.grad_buckets)
     views = [View(cams[i], dtf, targets[j]) for j, i in enumerate(mine)]
 
     def barrier():
@@ -325,7 +333,7 @@ def run_b200(args) -> None:
     barrier()
     clk = clocks.stop()
     ms = max_over_ranks(e0.elapsed_time(e1))
-    launches = trainer.launches - launches0 + args.steps * 1  # + Adam
+    launches = trainer.launches - launches0  # (lane sums, exchange and Adam included)
     ms_step = ms / args.steps
     value = 1000.0 / ms_step
     loss_val = float(loss.item())
@@ -503,7 +511,8 @@ def run_b200(args) -> None:
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": max(args.warmup, 3), "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f32+f64", "data": "synthetic (seeded, scenes.py)",
-            "config": config_block(world, args.backend, not args.no_graphs), "e2e": e2e, "render_mpx_s": render_mpx_s,
+            "config": config_block(world, args.backend, not args.no_graphs, args.grad_payload, args.grad_buckets),
+            "e2e": e2e, "render_mpx_s": render_mpx_s,
             "render_roofline": render_roof, "loss": loss_val,
             "gpu_launches": int(launches), "roofline": roof, "kernels": kernels, "stages": stages,
             "render_sweep_c3": sweep,
@@ -648,7 +657,8 @@ def run_c4(args, dev, rank, world) -> dict:
             targets[(k, i)] = fr.out_img.view(cams[i].height, cams[i].width, 3).clone()
     del rz, gt
     group = dist.group.WORLD if world > 1 else None
-    tr = Trainer(learned, TrainConfig(iterations=30000), group=group, graphs=not args.no_graphs)
+    tr = Trainer(learned, TrainConfig(iterations=30000), group=group, graphs=not args.no_graphs,
+                 grad_payload=args.grad_payload, grad_buckets=args.grad_buckets)
     tr.track_densify(True)
     view_sets = {k: [View(cams[i], tfs[k], targets[(k, i)]) for i in mine] for k in sorted(set(used))}
 

@@ -26,6 +26,8 @@
  *   vegs_loss_aux               loss.py:175-240 normal-consistency + bilateral-smoothness regularisers
  *   vegs_adam_step              train.py:176-195 adam_step (+ learning_rates :156-173 on the host)
  *   vegs_adam_step_sum          the same on the sum of the trainer's per-lane gradient buffers
+ *   vegs_grad_pack / vegs_adam_step_range  the view-sharded step's gradient exchange (no reference
+ *                               counterpart: the reference is single-process), bucketed by unit
  *   vegs_tf_eval                transfer.py:91-127 eval_opacity / eval_color / d_*_dv
  *   vegs_densify_count / _apply train.py:237-284 densify_and_prune (+ DensifyStats.add :210-214,
  *                               fused into vegs_preprocess_backward)
@@ -316,6 +318,22 @@ int vegs_adam_step(double *params, const double *grads, double *m, double *v, in
 int vegs_adam_step_sum(double *params, double *grads0, const double *grads1, const double *grads2,
                        const double *grads3, double *m, double *v, int64_t n, const double *hyper,
                        double grad_scale, int32_t *nonfinite, const int64_t *skip, void *stream);
+
+/* Gradient exchange of the view-sharded step, per bucket of units
+ * [unit0, unit0 + units) of the 19 n class-major layout (one unit = one parameter
+ * component, n values):
+ *   vegs_grad_pack: g = ((grads0 + grads1) + grads2) + grads3 over the non-NULL partials (the
+ *     order vegs_adam_step_sum uses), written to payload32 (float32, 19 n, same indexing)
+ *     when it is non-NULL, else back into grads0 -- the buffer the all-reduce then sums;
+ *   vegs_adam_step_range: Adam (hyper / skip as vegs_adam_step_sum) over the units on the
+ *     all-reduced gradient, read from payload32 (widened to float64 and stored into grads0)
+ *     or from grads0.
+ * Packing bucket b + 1 overlaps bucket b's all-reduce, which overlaps Adam on bucket b - 1. */
+int vegs_grad_pack(double *grads0, const double *grads1, const double *grads2, const double *grads3,
+                   float *payload32, int64_t n, int32_t unit0, int32_t units, void *stream);
+int vegs_adam_step_range(double *params, double *grads0, const float *payload32, double *m, double *v,
+                         int64_t n, int32_t unit0, int32_t units, const double *hyper, int32_t *nonfinite,
+                         const int64_t *skip, void *stream);
 
 /* Library build identity (for the loader's sanity check). */
 const char *vegs_version(void);

@@ -131,11 +131,12 @@ struct GradParts {
     int n_extra;
 };
 
-__global__ void __launch_bounds__(256) adam_kernel(double *params, GradParts gp, double *m, double *v, int64_t n,
-                                                   const double *lr, double grad_scale, double bias1, double bias2,
-                                                   int *nonfinite, const int64_t *skip) {
+__global__ void __launch_bounds__(256) adam_kernel(double *params, GradParts gp, const float *pay32, double *m,
+                                                   double *v, int64_t n, int unit0, const double *lr,
+                                                   double grad_scale, double bias1, double bias2, int *nonfinite,
+                                                   const int64_t *skip) {
     if (skip && skip[0]) return;  // a view of the step overflowed its buffers: the step is redone
-    const int unit = blockIdx.y;
+    const int unit = unit0 + (int)blockIdx.y;
     const int cls = kUnitClass[unit];
     const double b1 = 0.9, b2 = 0.999, eps = 1e-15;
     const double lr_c = params ? lr[cls] : 0.0;
@@ -146,8 +147,14 @@ __global__ void __launch_bounds__(256) adam_kernel(double *params, GradParts gp,
     const int64_t base = (int64_t)unit * n;
     for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x) {
         const int64_t i = base + j;
-        double gs = gp.g0[i];
-        if (gp.n_extra > 0) {
+        double gs;
+        if (pay32) {  // the all-reduced float32 payload, widened (and kept as the step gradient)
+            gs = (double)pay32[i];
+            gp.g0[i] = gs;
+        } else {
+            gs = gp.g0[i];
+        }
+        if (!pay32 && gp.n_extra > 0) {
             for (int k = 0; k < gp.n_extra; ++k) gs = gs + gp.g[k][i];
             gp.g0[i] = gs;
         }
@@ -166,6 +173,19 @@ __global__ void __launch_bounds__(256) adam_kernel(double *params, GradParts gp,
         const double upd = (mi / bias1) / (sqrt(vi / bias2) + eps);
         params[i] = params[i] - lr_c * upd;
     }
+}
+
+// Cross-rank exchange, first half: the lanes' partial gradients of units [unit0, unit0 +
+// gridDim.y) summed in the Adam kernel's fixed order, into g0 (float64 payload) or into a
+// float32 payload for the all-reduce.
+__global__ void __launch_bounds__(256) grad_pack_kernel(GradParts gp, float *pay32, int64_t n, int unit0) {
+    const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= n) return;
+    const int64_t i = (int64_t)(unit0 + (int)blockIdx.y) * n + j;
+    double gs = gp.g0[i];
+    for (int k = 0; k < gp.n_extra; ++k) gs = gs + gp.g[k][i];
+    if (pay32) pay32[i] = (float)gs;
+    else if (gp.n_extra > 0) gp.g0[i] = gs;
 }
 
 }  // namespace vegs
@@ -231,7 +251,8 @@ extern "C" int vegs_splat_table_from_arrays(const double *mean2d, const double *
 
 static int adam_launch(double *params, GradParts gp, double *m, double *v, int64_t n, const double *lr,
                        double grad_scale, double bias1, double bias2, int32_t *nonfinite, void *stream,
-                       const int64_t *skip = nullptr) {
+                       const int64_t *skip = nullptr, const float *pay32 = nullptr, int unit0 = 0,
+                       int units = 19) {
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -240,8 +261,8 @@ static int adam_launch(double *params, GradParts gp, double *m, double *v, int64
     // load-latency bound: 55% long-scoreboard stalls, 42% of HBM)
     const int bx = (int)((n + 255) / 256);
     (void)sms;
-    adam_kernel<<<dim3(bx, 19), 256, 0, (cudaStream_t)stream>>>(params, gp, m, v, n, lr, grad_scale, bias1, bias2,
-                                                                nonfinite, skip);
+    adam_kernel<<<dim3(bx, units), 256, 0, (cudaStream_t)stream>>>(params, gp, pay32, m, v, n, unit0, lr,
+                                                                   grad_scale, bias1, bias2, nonfinite, skip);
     VEGS_CHECK_LAUNCH();
     return VEGS_OK;
 }
@@ -266,6 +287,31 @@ extern "C" int vegs_adam_step_sum(double *params, double *grads0, const double *
         if (extra[k]) gp.g[gp.n_extra++] = extra[k];
     if (n == 0 || (!params && gp.n_extra == 0)) return VEGS_OK;
     return adam_launch(params, gp, m, v, n, hyper, grad_scale, NAN, NAN, nonfinite, stream, skip);
+}
+
+extern "C" int vegs_grad_pack(double *grads0, const double *grads1, const double *grads2, const double *grads3,
+                              float *payload32, int64_t n, int32_t unit0, int32_t units, void *stream) {
+    if (unit0 < 0 || units < 0 || unit0 + units > 19) return VEGS_ERR_ARG;
+    if (n > 0 && units > 0 && !grads0) return VEGS_ERR_ARG;
+    const double *extra[3] = {grads1, grads2, grads3};
+    GradParts gp{grads0, {nullptr, nullptr, nullptr}, 0};
+    for (int k = 0; k < 3; ++k)
+        if (extra[k]) gp.g[gp.n_extra++] = extra[k];
+    if (n == 0 || units == 0 || (!payload32 && gp.n_extra == 0)) return VEGS_OK;
+    grad_pack_kernel<<<dim3((unsigned)((n + 255) / 256), units), 256, 0, (cudaStream_t)stream>>>(gp, payload32, n,
+                                                                                                 unit0);
+    VEGS_CHECK_LAUNCH();
+    return VEGS_OK;
+}
+
+extern "C" int vegs_adam_step_range(double *params, double *grads0, const float *payload32, double *m, double *v,
+                                    int64_t n, int32_t unit0, int32_t units, const double *hyper,
+                                    int32_t *nonfinite, const int64_t *skip, void *stream) {
+    if (unit0 < 0 || units < 0 || unit0 + units > 19) return VEGS_ERR_ARG;
+    if (n > 0 && units > 0 && (!params || !grads0 || !m || !v || !hyper || !nonfinite)) return VEGS_ERR_ARG;
+    if (n == 0 || units == 0) return VEGS_OK;
+    GradParts gp{grads0, {nullptr, nullptr, nullptr}, 0};
+    return adam_launch(params, gp, m, v, n, hyper, 1.0, NAN, NAN, nonfinite, stream, skip, payload32, unit0, units);
 }
 
 // ---------------------------------------------------------------------------------

@@ -52,6 +52,8 @@ LAUNCHES = {
     "vegs_loss_aux": 3,
     "vegs_adam_step": 1,
     "vegs_adam_step_sum": 1,
+    "vegs_grad_pack": 1,
+    "vegs_adam_step_range": 1,
     "vegs_densify_count": 3,
     "vegs_densify_apply": 1,
 }
@@ -535,6 +537,21 @@ def adam_step_sum_device(params, grads, m, v, n: int, hyper: torch.Tensor, nonfi
     ex = list(extra_grads) + [None] * (3 - len(extra_grads))
     call("vegs_adam_step_sum", _p(params), _p(grads), _p(ex[0]), _p(ex[1]), _p(ex[2]), _p(m), _p(v), n, _p(hyper),
          1.0, _p(nonfinite), _p(skip), _stream())
+
+
+def grad_pack_device(grads, extra_grads, payload32, n: int, unit0: int, units: int) -> None:
+    """Sum the lanes' partial gradients of units [unit0, unit0 + units) (fixed order) into
+    ``payload32`` (float32) or, when it is None, into ``grads``."""
+    ex = list(extra_grads) + [None] * (3 - len(extra_grads))
+    call("vegs_grad_pack", _p(grads), _p(ex[0]), _p(ex[1]), _p(ex[2]), _p(payload32), n, unit0, units, _stream())
+
+
+def adam_step_range_device(params, grads, payload32, m, v, n: int, unit0: int, units: int, hyper: torch.Tensor,
+                           nonfinite: torch.Tensor, skip: torch.Tensor | None = None) -> None:
+    """Adam over units [unit0, unit0 + units) on the exchanged gradient (``payload32`` when
+    given, widened into ``grads``; else ``grads``)."""
+    call("vegs_adam_step_range", _p(params), _p(grads), _p(payload32), _p(m), _p(v), n, unit0, units, _p(hyper),
+         _p(nonfinite), _p(skip), _stream())
 
 
 class RenderPipeline:

@@ -25,7 +25,7 @@ import torch
 from .constants import DEFAULT_SETTINGS, RasterSettings
 from .device import DeviceTF, Rasterizer, adam_step_device, adam_step_sum_device, require_cuda, use_stream
 from .model import PARAM_CLASSES, GaussianSet, class_offsets
-from .parallel import allreduce_gradients
+from .parallel import GradientExchange, allreduce_gradients
 
 ADAM_BETA1 = 0.9
 ADAM_BETA2 = 0.999
@@ -196,7 +196,8 @@ class Trainer:
 
     def __init__(self, gs: GaussianSet, config: TrainConfig, settings: RasterSettings = DEFAULT_SETTINGS,
                  background=(1.0, 1.0, 1.0), l1_weight: float | None = None, group=None, with_aux: bool = False,
-                 lanes: int = 4, fast_t: bool = False, graphs: bool = False):
+                 lanes: int = 4, fast_t: bool = False, graphs: bool = False, grad_payload: str = "f64",
+                 grad_buckets: int = 4):
         self.device = require_cuda()
         # fast_t: the forward carries T in float32 with every skip / clamp / termination
         # decision exact (vegs_composite_forward_fast).  Default: the float64 chain, which
@@ -218,6 +219,9 @@ class Trainer:
         # smoothness regularisers, as the reference's loop does (train.py:476-479)
         self.with_aux = with_aux
         self.group = group
+        # with a process group: the bucketed, pipelined gradient exchange (parallel.py)
+        self.exchange = (GradientExchange(self.n, self.device, group, grad_payload, grad_buckets)
+                         if group is not None else None)
         self.densify_stats = None  # (n, 5) float64 when densification is tracked
         # Views are pipelined over `lanes` CUDA streams, each with its own scratch pool,
         # loss workspace and gradient buffer: one view's preprocess, count readback and
@@ -237,6 +241,7 @@ class Trainer:
         self._graphs: dict = {}
         self._graph_pool = None
         self._replayed_launches = 0
+        self._update_launches = 0  # lane sums, exchange and Adam launches
         self.graph_stats = {"captures": 0, "replays": 0, "redos": 0}
         # [overflow, max instances, max kept splats] of the views of the current step
         self._state = torch.zeros(3, dtype=torch.int64, device=self.device)
@@ -264,7 +269,8 @@ class Trainer:
     @property
     def launches(self) -> int:
         """Kernels launched by this trainer's steps (graph replays count their captured kernels)."""
-        return sum(lane.rz.launches + lane.loss_launches for lane in self.lanes) + self._replayed_launches
+        return (sum(lane.rz.launches + lane.loss_launches for lane in self.lanes) + self._replayed_launches
+                + self._update_launches)
 
     def gaussians(self) -> GaussianSet:
         return GaussianSet.unpack(self.params.cpu().numpy(), self.n)
@@ -403,12 +409,18 @@ class Trainer:
         # the lanes' partial sums are added inside the Adam kernel (fixed lane order), or in
         # a sum-only pass of the same kernel before a cross-rank all-reduce
         extra = [lane.grads for k, lane in enumerate(lanes) if k and used[k]]
-        while len(extra) > 3 or (extra and self.group is not None):
+        while len(extra) > 3:
             adam_step_device(None, self.grads, None, None, self.n, None, 1.0, 1, None, extra[:3])
             extra = extra[3:]
-        allreduce_gradients(self.grads, self.group)
-        adam_step_sum_device(self.params, self.grads, self.m, self.v, self.n, hyper, self.nonfinite, extra,
-                             skip=state)
+            self._update_launches += 1
+        if self.exchange is not None:  # cross-rank: pack / all-reduce / Adam per bucket
+            before = self.exchange.launches
+            self.exchange.step(self.params, self.grads, extra, self.m, self.v, hyper, self.nonfinite, skip=state)
+            self._update_launches += self.exchange.launches - before
+        else:
+            adam_step_sum_device(self.params, self.grads, self.m, self.v, self.n, hyper, self.nonfinite, extra,
+                                 skip=state)
+            self._update_launches += 1
         if state is not None:
             self._state_host.copy_(state, non_blocking=True)
         if not views:
@@ -479,11 +491,11 @@ class Trainer:
         cap_stream = torch.cuda.Stream(self.device)
         cap_stream.wait_stream(main)
         g = torch.cuda.CUDAGraph()
-        before = sum(lane.rz.launches + lane.loss_launches for lane in self.lanes)
+        before = self.launches
         with torch.cuda.graph(g, stream=cap_stream, pool=self._graph_pool):
             loss = self._step_body(views, total, self._hyper_dev, self._state)
         main.wait_stream(cap_stream)
-        captured = sum(lane.rz.launches + lane.loss_launches for lane in self.lanes) - before
+        captured = self.launches - before
         self._replayed_launches -= captured  # the capture itself launched nothing; replays count them
         self._graphs[key] = (g, loss, captured)
         self.graph_stats["captures"] += 1
@@ -522,6 +534,9 @@ class Trainer:
         self._graphs.clear()  # captured with the old buffers
         self.grads = torch.zeros_like(self.params)
         self.densify_stats = torch.zeros(self.n * 5, dtype=torch.float64, device=self.device)
+        if self.exchange is not None:
+            ex = self.exchange
+            self.exchange = GradientExchange(self.n, self.device, self.group, ex.payload, len(ex.bounds))
         return n_out
 
     def reset_weights(self) -> None:

@@ -70,3 +70,17 @@ def test_sharded_gradients_equal_single_process_mean(world):
     for r in res[1:]:
         assert np.array_equal(r, res[0])  # replicas stay identical
     assert np.abs(res[0] - full).max() <= 1e-12 * max(np.abs(full).max(), 1.0)
+
+
+def test_gradient_exchange_buckets_cover_the_units():
+    """The exchange's unit ranges tile the 19 units of the class-major buffer in order."""
+    from paper_2504_13339_b200.parallel import GradientExchange
+
+    for b in (1, 2, 3, 4, 7, 19, 40):
+        ex = GradientExchange(5, "cpu", payload="f64", buckets=b)
+        flat = [u for lo, hi in ex.bounds for u in range(lo, hi)]
+        assert flat == list(range(19)) and all(hi > lo for lo, hi in ex.bounds)
+        assert len(ex.bounds) == min(b, 19) and ex.pay32 is None
+    assert GradientExchange(5, "cpu", payload="f32").pay32.dtype == torch.float32
+    with pytest.raises(ValueError):
+        GradientExchange(5, "cpu", payload="bf16")

@@ -581,8 +581,23 @@ def test_trainer_nccl_group_of_one():
         assert torch.equal(allreduce_gradients(g.clone(), dist.group.WORLD), g)
         a = Trainer(learned, TrainConfig(iterations=100), group=dist.group.WORLD)
         la = float(a.step(views, iteration=1).item())
+        # the bucketed exchange: float64 payload at any bucket count, float32 payload
+        other = {}
+        for payload, buckets in (("f64", 1), ("f64", 19), ("f32", 4)):
+            t = Trainer(learned, TrainConfig(iterations=100), group=dist.group.WORLD, grad_payload=payload,
+                        grad_buckets=buckets)
+            other[payload, buckets] = (float(t.step(views, iteration=1).item()), t.params.clone(), t.grads.clone(),
+                                       t.exchange.collectives)
     finally:
         dist.destroy_process_group()
     b = Trainer(learned, TrainConfig(iterations=100))
     lb = float(b.step(views, iteration=1).item())
     assert la == lb and torch.equal(a.params, b.params)
+    assert a.exchange.collectives == 4  # one all-reduce per bucket
+    for (payload, buckets), (l, p, g, coll) in other.items():
+        assert l == lb and coll == buckets
+        if payload == "f64":
+            assert torch.equal(p, b.params) and torch.equal(g, b.grads)
+        else:  # the step gradient rounded to float32 once, then widened
+            assert torch.equal(g, b.grads.float().double())
+            assert (p - b.params).abs().max().item() <= 1e-5 * TrainConfig().lr_weight  # largest lr
