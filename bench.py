@@ -68,6 +68,8 @@ def parse():
     ap.add_argument("--c4-steps", type=int, default=20)
     ap.add_argument("--sweep-frames", type=int, default=2)
     ap.add_argument("--lanes", type=int, default=4, help="CUDA-stream lanes of the view pipeline")
+    ap.add_argument("--no-cull", action="store_true",
+                    help="bin on the reference's whole rects (default: tight ellipse boxes, identical results)")
     ap.add_argument("--no-graphs", action="store_true",
                     help="host-counted eager steps instead of device-count steps replayed as CUDA graphs")
     ap.add_argument("--backend", choices=("nccl", "gloo"), default="nccl",
@@ -186,15 +188,16 @@ STAGES = ("vegs_preprocess_forward", "vegs_bin_count", "vegs_bin_sort", "vegs_co
           "vegs_loss_l1_ssim", "vegs_composite_backward", "vegs_preprocess_backward")
 
 
-def stage_bytes(name: str, n: int, n_kept: int, n_inst: int, pixels: int) -> float | None:
+def stage_bytes(name: str, n: int, n_kept: int, n_inst: int, pixels: int, listed: float = 1.0) -> float | None:
     """Algorithmic HBM bytes per call (with this build's float64
-    parameters and float32 splat table); None where no byte model bounds the stage."""
+    parameters and float32 splat table); None where no byte model bounds the stage.
+    ``listed``: tile-list entries per reference instance (culled binning, < 1)."""
     if name == "vegs_preprocess_forward":  # params in; record 48 + rect 16 + tiles 4 + depth key 8 out
         return float(152 * n + 76 * n)
     if name == "vegs_bin_sort":  # splat ids in depth order + rects in, one id per instance out
-        return float(20 * n_kept + 4 * n_inst)
+        return float(20 * n_kept + 4 * n_inst * listed)
     if name in ("vegs_composite_forward", "vegs_composite_forward_fast", "vegs_composite_backward"):
-        return algorithmic_bytes(name, n_kept, n_inst, pixels)
+        return algorithmic_bytes(name, n_kept, n_inst, pixels, listed=listed)
     if name == "vegs_loss_l1_ssim":  # image + target in, gradient out (fused minimum)
         return float(36 * pixels)
     if name == "vegs_preprocess_backward":  # params in, gradients read+written, row sums
@@ -202,7 +205,8 @@ def stage_bytes(name: str, n: int, n_kept: int, n_inst: int, pixels: int) -> flo
     return None
 
 
-def composite_roofline(ksum: dict, pixels: int, ncu_key: str, ncu_file: str = "ncu_composite.json") -> dict | None:
+def composite_roofline(ksum: dict, pixels: int, ncu_key: str, ncu_file: str = "ncu_composite.json",
+                       listed: float = 1.0) -> dict | None:
     """Roofline of the compositing forward from a KernelTimer summary: algorithmic HBM
     bytes / live CUDA-event launch time against MEASURED_PEAKS' HBM, plus
     the issue roofline (warp instructions per launch from the committed ncu capture, scaled
@@ -217,12 +221,13 @@ def composite_roofline(ksum: dict, pixels: int, ncu_key: str, ncu_file: str = "n
     if rec is None:
         return None
     peak, peak_kind = peaks()
-    byts = [algorithmic_bytes("vegs_composite_forward", nk, ni, pixels) for nk, ni in rec["counts"]]
+    byts = [algorithmic_bytes("vegs_composite_forward", nk, ni, pixels, listed=listed) for nk, ni in rec["counts"]]
     achieved = sum(byts) / len(byts) / (rec["avg_ms"] / 1000.0) / 1e9
     out = {"bound": "hbm", "kernel": "vegs_composite_forward", "achieved": achieved, "peak": peak,
            "peak_source": peak_kind, "unit": "GB/s", "frac": achieved / peak, "traffic": None,
            "algorithmic_bytes_per_launch": sum(byts) / len(byts), "avg_launch_ms": rec["avg_ms"],
-           "launches": rec["launches"], "avg_instances": sum(c[1] for c in rec["counts"]) / len(rec["counts"])}
+           "launches": rec["launches"], "avg_instances": sum(c[1] for c in rec["counts"]) / len(rec["counts"]),
+           "listed_fraction": listed}
     prof = ROOT / "profiles" / ncu_file
     if prof.exists():
         r = json.loads(prof.read_text()).get(ncu_key)
@@ -257,11 +262,14 @@ def composite_roofline(ksum: dict, pixels: int, ncu_key: str, ncu_file: str = "n
     return out
 
 
-def algorithmic_bytes(name: str, n_kept: int, n_inst: int, pixels: int, n_ch: int = 3) -> float:
-    """SURVEY.md §8(d) minimum HBM bytes per composite launch."""
+def algorithmic_bytes(name: str, n_kept: int, n_inst: int, pixels: int, n_ch: int = 3,
+                      listed: float = 1.0) -> float:
+    """SURVEY.md §8(d) minimum HBM bytes per composite launch, over the instances the
+    launch actually walks: n_inst reference instances x ``listed`` (the culled binning's
+    tile-list entries per reference instance, measured)."""
     per_inst = 4 + 28 + 4 * n_ch
     per_px = 4 * n_ch + 4 + 4
-    b = n_inst * per_inst + pixels * per_px
+    b = n_inst * listed * per_inst + pixels * per_px
     if name == "vegs_composite_backward":
         b += n_kept * (6 + n_ch) * 4 * 2
     return float(b)
@@ -299,7 +307,8 @@ def run_b200(args) -> None:
 
     group = dist.group.WORLD if world > 1 else None
     trainer = Trainer(learned, TrainConfig(iterations=30000), group=group, lanes=args.lanes,
-                      graphs=not args.no_graphs, grad_payload=args.grad_payload, grad_buckets=args.grad_buckets)
+                      graphs=not args.no_graphs, grad_payload=args.grad_payload, grad_buckets=args.grad_buckets,
+                      cull=not args.no_cull)
     views = [View(cams[i], dtf, targets[j]) for j, i in enumerate(mine)]
 
     def barrier():
@@ -365,25 +374,30 @@ def run_b200(args) -> None:
     from paper_2504_13339_b200.device import LossKernel
 
     stage_timer = KernelTimer(None, names=STAGES)
-    srz = Rasterizer(pooled=True, fast_t=trainer.fast_t)
+    srz = Rasterizer(pooled=True, fast_t=trainer.fast_t, cull=trainer.cull)
     srz.contrib_counts = False
     sloss = LossKernel(dev)
     sgrads = torch.zeros_like(trainer.params)
     ssums = torch.zeros(2, dtype=torch.float64, device=dev)
     d_img = torch.empty(1024, 1024, 3, dtype=torch.float32, device=dev)
+    listed_n = [0, 0]  # (tile-list entries, reference instances) of the profiled views
     for rep in range(2):  # the first pass grows the pools
         srz.timer = stage_timer if rep else None
         sloss.timer = stage_timer if rep else None
         for v in views[:4]:
             fr = srz.forward(trainer.params, trainer.n, v.tf, v.camera)
+            if rep:
+                listed_n[0] += int(fr.tile_end[-1])  # serialised pass: the read costs nothing timed
+                listed_n[1] += int(fr.n_inst)
             sloss(fr.out_img.view(1024, 1024, 3), v.target, 0.8, 0.2, d_img, ssums)
             srz.backward(fr, d_img, None, sgrads, accumulate=True)
     torch.cuda.synchronize()
     stage_timer.rz = srz
+    listed = listed_n[0] / max(listed_n[1], 1)
     peak_hbm, _ = peaks()
     stages = {}
     for name, rec in stage_timer.summary().items():
-        byts = [stage_bytes(name, trainer.n, nk, ni, 1024 * 1024) for nk, ni in rec["counts"]]
+        byts = [stage_bytes(name, trainer.n, nk, ni, 1024 * 1024, listed) for nk, ni in rec["counts"]]
         st = {"avg_ms": rec["avg_ms"], "calls": rec["launches"]}
         if byts and byts[0] is not None:
             gbs = sum(byts) / len(byts) / (rec["avg_ms"] / 1000.0) / 1e9
@@ -394,7 +408,7 @@ def run_b200(args) -> None:
     # ---- forward render throughput over the same views (the render pipeline's stream lanes)
     from paper_2504_13339_b200.device import RenderPipeline
 
-    pipe = RenderPipeline(lanes=args.lanes)
+    pipe = RenderPipeline(lanes=args.lanes, cull=not args.no_cull)
     items = [(v.camera, dtf) for v in views]
     for _ in range(2):
         pipe.render(trainer.params, trainer.n, items)
@@ -418,7 +432,7 @@ def run_b200(args) -> None:
     torch.cuda.synchronize()
     for _, rz in pipe.lanes:
         rz.timer = None
-    render_roof = composite_roofline(rtimer.summary(), 1024 * 1024, "vegs_composite_forward")
+    render_roof = composite_roofline(rtimer.summary(), 1024 * 1024, "vegs_composite_forward", listed=listed)
     del pipe
 
     # ---- end to end through the public API with host buffers: the views carry their
@@ -468,7 +482,7 @@ def run_b200(args) -> None:
     roof = None
     if dom:
         rec = ksum[dom]
-        byts = [algorithmic_bytes(dom, nk, ni, 1024 * 1024) for nk, ni in rec["counts"]]
+        byts = [algorithmic_bytes(dom, nk, ni, 1024 * 1024, listed=listed) for nk, ni in rec["counts"]]
         avg_bytes = sum(byts) / len(byts)
         achieved = avg_bytes / (rec["avg_ms"] / 1000.0) / 1e9
         traffic, issue = None, None
@@ -494,6 +508,7 @@ def run_b200(args) -> None:
         roof = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "peak_source": peak_kind,
                 "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
                 "algorithmic_bytes_per_launch": avg_bytes, "avg_launch_ms": rec["avg_ms"],
+                "listed_fraction": listed,
                 "share_of_step": rec["total_ms"] / ktimed_ms,
                 "timing": f"CUDA events on the launching lane stream over a separate {k_steps}-step pass "
                           "identical to the timed region",
@@ -593,7 +608,7 @@ def run_sweep(args, dev, rank, world) -> dict:
     tfs = {f: [DeviceTF(scenes.random_tf(1000 + 8 * f + k), dev) for k in range(8)] for f in mine}
     from paper_2504_13339_b200.device import RenderPipeline
 
-    pipe = RenderPipeline(lanes=args.lanes)
+    pipe = RenderPipeline(lanes=args.lanes, cull=not args.no_cull)
     items = [(cams[f], tf) for f in mine for tf in tfs[f]]
     # warm-up over every (frame, TF): the scratch pools grow to the largest instance count
     # here, so no allocation happens inside the timed region
@@ -617,11 +632,13 @@ def run_sweep(args, dev, rank, world) -> dict:
     stimer = KernelTimer(None)
     for _, rz in pipe.lanes:
         rz.timer = stimer
-    pipe.render(params, len(gs), items)
+    listed = []
+    pipe.render(params, len(gs), items, on_frame=lambda i, fr: listed.append((fr.tile_end[-1].clone(), fr.n_inst)))
     torch.cuda.synchronize()
     for _, rz in pipe.lanes:
         rz.timer = None
-    roof = composite_roofline(stimer.summary(), 1920 * 1080, "vegs_composite_forward_c3")
+    lf = sum(int(t) for t, _ in listed) / max(sum(n for _, n in listed), 1)
+    roof = composite_roofline(stimer.summary(), 1920 * 1080, "vegs_composite_forward_c3", listed=lf)
     return {"workload": "c3: 3M blob-shaped Gaussians, 1920x1080, 8 random 256-knot TFs per frame (1-6 bumps), "
                         "forward render per (frame, TF), frames sharded across ranks",
             "renders": renders, "ms_per_render": ms / (renders / world), "mpx_s": renders * 1920 * 1080 / (ms / 1e3) / 1e6,
@@ -658,7 +675,7 @@ def run_c4(args, dev, rank, world) -> dict:
     del rz, gt
     group = dist.group.WORLD if world > 1 else None
     tr = Trainer(learned, TrainConfig(iterations=30000), group=group, graphs=not args.no_graphs,
-                 grad_payload=args.grad_payload, grad_buckets=args.grad_buckets)
+                 grad_payload=args.grad_payload, grad_buckets=args.grad_buckets, cull=not args.no_cull)
     tr.track_densify(True)
     view_sets = {k: [View(cams[i], tfs[k], targets[(k, i)]) for i in mine] for k in sorted(set(used))}
 

@@ -144,13 +144,19 @@ int vegs_bin_count(const uint32_t *tiles, int64_t n, int64_t *offsets, int64_t *
  * (duplicate-order index) and order (kept index, the reference's `order`);
  * tile_start/tile_end (n_tiles); optional tile_order (n_tiles): tile ids by decreasing
  * instance count, the launch order the compositing kernels accept (scheduling only).
- * n_inst must be < 2^31 (int32 instance positions); larger views return VEGS_ERR_ARG. */
+ * n_inst must be < 2^31 (int32 instance positions); larger views return VEGS_ERR_ARG.
+ * cull_record (nullable; float32 splat table of n_channels, counting-placement path only,
+ * inst_pid / order must be NULL): bin each splat on its rect clipped to the tight bounding
+ * box of its pass ellipse {pw >= pmin} instead of the whole rect.  The tile lists then hold
+ * only instances that can blend in their tile (about 3/4 of them): images, T, contributor
+ * counts and gradients are identical, tile_start / tile_end / out_last index the shorter
+ * lists, and sorted_gauss needs at most n_inst entries.  NULL: the reference's lists. */
 int vegs_bin_sort(const uint32_t *tiles, const uint64_t *depth_key, const int32_t *rect,
                   const int64_t *offsets, const int64_t *kept_idx, int64_t n, int64_t n_kept,
                   int64_t n_inst, int32_t width, int32_t height, int32_t tile_size,
                   uint32_t *sorted_gauss, uint32_t *inst_pid, int64_t *order,
-                  int32_t *tile_start, int32_t *tile_end, int32_t *tile_order, void *ws,
-                  size_t *ws_bytes, void *stream);
+                  int32_t *tile_start, int32_t *tile_end, int32_t *tile_order,
+                  const float *cull_record, int32_t n_channels, void *ws, size_t *ws_bytes, void *stream);
 
 /* Device-count binning (no host round trip per view; CUDA-graph capturable).
  * vegs_bin_count_dev = vegs_bin_count, then: step_state[1] = max(step_state[1], n_instances),
@@ -161,15 +167,16 @@ int vegs_bin_sort(const uint32_t *tiles, const uint64_t *depth_key, const int32_
  * is therefore read-write.  Same ws as vegs_bin_count.
  * vegs_bin_sort_dev = vegs_bin_sort's counting placement with n_kept read from counts
  * (device); launches and the workspace are sized for kept_capacity kept splats.  Views
- * above 12288 tiles need the radix path and host counts: VEGS_ERR_ARG. */
+ * above 12288 tiles need the radix path and host counts: VEGS_ERR_ARG.  cull_record as
+ * in vegs_bin_sort. */
 int vegs_bin_count_dev(uint32_t *tiles, int64_t n, int64_t *offsets, int64_t *kept_idx, int64_t *counts,
                        int64_t inst_capacity, int64_t kept_capacity, int64_t *step_state, int32_t *poison,
                        void *ws, size_t *ws_bytes, void *stream);
 int vegs_bin_sort_dev(const uint64_t *depth_key, const int32_t *rect, const int64_t *offsets,
                       const int64_t *kept_idx, int64_t n, const int64_t *counts, int64_t kept_capacity,
                       int32_t width, int32_t height, int32_t tile_size, uint32_t *sorted_gauss,
-                      int32_t *tile_start, int32_t *tile_end, int32_t *tile_order, void *ws,
-                      size_t *ws_bytes, void *stream);
+                      int32_t *tile_start, int32_t *tile_end, int32_t *tile_order, const float *cull_record,
+                      int32_t n_channels, void *ws, size_t *ws_bytes, void *stream);
 
 /* ---- composite -------------------------------------------------------------------- */
 /* Tile blend on the splat table.  out_img H x W x C, out_t H x W (storage type),

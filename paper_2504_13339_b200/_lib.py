@@ -56,7 +56,7 @@ _SIGS = {
                                      POINTER(VegsSplatTable), P],
     "vegs_bin_count": [P, c_int64, P, P, P, P, POINTER(c_size_t), P],
     "vegs_bin_sort": [P, P, P, P, P, c_int64, c_int64, c_int64, c_int32, c_int32, c_int32, P, P, P, P, P, P, P,
-                      POINTER(c_size_t), P],
+                      c_int32, P, POINTER(c_size_t), P],
     "vegs_composite_forward": [P, P, P, P, P, c_int32, c_int32, P, c_int32, c_int32, c_double, c_double,
                                P, P, P, P, P, P],
     "vegs_composite_forward_fast": [P, P, P, P, P, c_int32, P, c_int32, c_int32, c_double, c_double, P, P, P, P,
@@ -80,8 +80,8 @@ _SIGS = {
     "vegs_grad_pack": [P, P, P, P, P, c_int64, c_int32, c_int32, P],
     "vegs_adam_step_range": [P, P, P, P, P, c_int64, c_int32, c_int32, P, P, P, P],
     "vegs_bin_count_dev": [P, c_int64, P, P, P, c_int64, c_int64, P, P, P, POINTER(c_size_t), P],
-    "vegs_bin_sort_dev": [P, P, P, P, c_int64, P, c_int64, c_int32, c_int32, c_int32, P, P, P, P, P,
-                          POINTER(c_size_t), P],
+    "vegs_bin_sort_dev": [P, P, P, P, c_int64, P, c_int64, c_int32, c_int32, c_int32, P, P, P, P, P, c_int32,
+                          P, POINTER(c_size_t), P],
 }
 
 _lib = None

@@ -209,6 +209,37 @@ __global__ void tile_weight_kernel(const int32_t *tile_start, const int32_t *til
     val[t] = t;
 }
 
+// Culled binning rectangles (float32 tables, training / render paths): the reference's rect
+// clipped to the tight bounding box of the instance's pass ellipse.  A pixel blends only if
+// pw >= pmin, i.e. q = -2 pw = a dx^2 + 2 b dx dy + c dy^2 <= qmax = -2 pmin; on that ellipse
+// |dx| <= sqrt(qmax c / det) and |dy| <= sqrt(qmax a / det), det = a c - b^2.  The float64
+// decisions of the compositing kernels use exactly these float32 record values, so a box
+// inflated by 5e-4 relative + 1e-3 px over the float32 evaluation (det > 1e-2 a c keeps its
+// relative error below 4e-5) holds every passing pixel: the tile lists lose only instances
+// that cannot blend in the tile (23% at c2 / c3), images, T, contributor counts and
+// gradients are unchanged.  Conics not clearly positive definite keep the full rect.
+__global__ void bin_rect_kernel(const float *record, int rs, const int4 *rect, int64_t n, int4 *brect) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    int4 r = rect[i];
+    if (r.y > r.x && r.w > r.z) {
+        const float *g = record + (int64_t)rs * i;
+        const float mx = g[0], my = g[1], a = g[2], b = g[3], c = g[4], pm = g[6];
+        const float det = a * c - b * b;
+        if (a > 0.f && c > 0.f && det > 1e-2f * (a * c) && pm <= 0.f && isfinite(mx) && isfinite(my)) {
+            const float qmax = -2.f * pm;
+            const float rx = sqrtf(qmax * c / det) * 1.0005f + 1e-3f, ry = sqrtf(qmax * a / det) * 1.0005f + 1e-3f;
+            // first / last pixel whose centre x + 0.5 lies within mx -/+ rx, clamped to the rect
+            // in float before the int conversion
+            const float xl = fmaxf(ceilf(mx - rx - 0.5f), (float)r.x), xh = fminf(floorf(mx + rx - 0.5f), (float)(r.y - 1));
+            const float yl = fmaxf(ceilf(my - ry - 0.5f), (float)r.z), yh = fminf(floorf(my + ry - 0.5f), (float)(r.w - 1));
+            if (!(xl <= xh && yl <= yh)) r = make_int4(0, 0, 0, 0);
+            else r = make_int4((int)xl, (int)xh + 1, (int)yl, (int)yh + 1);
+        }
+    }
+    brect[i] = r;
+}
+
 // ---- counting placement (no instance-level sort) ----------------------------------
 // The kept splats in depth order are cut into chunks of C.  (1) per chunk, per-tile
 // instance counts from a 2D difference array of the splats' tile rectangles; (2) those
@@ -227,6 +258,7 @@ __global__ void chunk_count_kernel(const uint32_t *ids, const int4 *rect, int64_
     const int64_t lo = (int64_t)c * C, hi = lo + C < n_kept ? lo + C : n_kept;
     for (int64_t r = lo + threadIdx.x; r < hi; r += blockDim.x) {
         const int4 q = __ldg(rect + ids[r]);
+        if (q.y <= q.x || q.w <= q.z) continue;  // a culled-empty binning rect
         const int x0 = q.x / kTile, x1 = (q.y - 1) / kTile + 1, y0 = q.z / kTile, y1 = (q.w - 1) / kTile + 1;
         atomicAdd(&diff[y0 * W1 + x0], 1);
         atomicAdd(&diff[y0 * W1 + x1], -1);
@@ -331,7 +363,7 @@ __global__ void __launch_bounds__(32 * kBands) place_kernel(const uint32_t *ids,
         if (r0 + 32 < hi) fetch(r0 + 32, g_n, q_n);
         const int x0 = q.x / kTile, nx = (q.y - 1) / kTile - x0 + 1;
         const int ys = max(q.z / kTile, band_lo), ye = min((q.w - 1) / kTile, band_hi);
-        const int cnt = r0 + lane < hi && ys <= ye ? nx * (ye - ys + 1) : 0;
+        const int cnt = r0 + lane < hi && ys <= ye && q.x < q.y ? nx * (ye - ys + 1) : 0;
         const float inx = 1.0f / (float)nx;
         unsigned todo = __ballot_sync(0xffffffffu, cnt > 0);  // splats of the group touching this band
         while (todo) {
@@ -555,7 +587,8 @@ static int bin_place_impl(const uint64_t *depth_key, const int32_t *rect, const 
                           const int64_t *kept_idx, int64_t n, int64_t n_kept, int64_t n_inst, int tiles_x,
                           int tiles_y, uint32_t *sorted_gauss, uint32_t *inst_pid, int64_t *order,
                           int32_t *tile_start, int32_t *tile_end, int32_t *tile_order, void *ws, size_t *ws_bytes,
-                          cudaStream_t s, const int64_t *counts_dev = nullptr) {
+                          cudaStream_t s, const int64_t *counts_dev = nullptr, const float *cull_record = nullptr,
+                          int rs = 0) {
     // counts_dev (device-count binning): n_kept / n_inst live on the device; every launch is
     // sized for n kept splats and the kernels read the real count (no host sync)
     const int64_t *n_kept_dev = counts_dev;
@@ -586,13 +619,15 @@ static int bin_place_impl(const uint64_t *depth_key, const int32_t *rect, const 
     const size_t b_n = align_up(sizeof(uint32_t) * (n + 1)), b_t = align_up(sizeof(uint32_t) * n_tiles);
     const size_t b_cnt = align_up(sizeof(uint32_t) * (size_t)n_chunks * n_tiles);
     const size_t b_grp = align_up(sizeof(uint32_t) * (size_t)n_groups * n_tiles);
-    const size_t need = 4 * b_n + b_cnt + b_grp + 4 * b_t + align_up(t_max);
+    const size_t b_rect = cull_record ? align_up(sizeof(int4) * n) : 0;
+    const size_t need = 4 * b_n + b_cnt + b_grp + 4 * b_t + align_up(t_max) + b_rect;
     if (!ws) {
         *ws_bytes = need;
         return VEGS_OK;
     }
     if (*ws_bytes < need) return VEGS_ERR_CAPACITY;
     char *w = (char *)ws;
+    int4 *brect = (int4 *)w; w += b_rect;
     uint32_t *dk0 = (uint32_t *)w; w += b_n;
     uint32_t *dk1 = (uint32_t *)w; w += b_n;
     uint32_t *id0 = (uint32_t *)w; w += b_n;
@@ -626,10 +661,16 @@ static int bin_place_impl(const uint64_t *depth_key, const int32_t *rect, const 
                                                                      n_kept_dev);
         VEGS_CHECK_LAUNCH();
         const uint32_t *ids = dv.Current();
+        const int4 *bin_rect = (const int4 *)rect;
+        if (cull_record) {  // the tight binning rects (all n splats: culled ones are never read)
+            bin_rect_kernel<<<(int)((n + 255) / 256), 256, 0, s>>>(cull_record, rs, (const int4 *)rect, n, brect);
+            VEGS_CHECK_LAUNCH();
+            bin_rect = brect;
+        }
         // 2. per-chunk tile counts -> first slot of every chunk in every tile, tile ranges
         const size_t diff_bytes = sizeof(int) * (size_t)(tiles_x + 1) * (tiles_y + 1);
-        chunk_count_kernel<<<n_chunks, 256, diff_bytes, s>>>(ids, (const int4 *)rect, n_kept, C, tiles_x, tiles_y,
-                                                             counts, n_kept_dev);
+        chunk_count_kernel<<<n_chunks, 256, diff_bytes, s>>>(ids, bin_rect, n_kept, C, tiles_x, tiles_y, counts,
+                                                             n_kept_dev);
         VEGS_CHECK_LAUNCH();
         const int64_t ng = (int64_t)n_groups * n_tiles;
         chunk_group_sum_kernel<<<(int)((ng + 255) / 256), 256, 0, s>>>(counts, n_chunks, n_tiles, G, gsum);
@@ -643,15 +684,15 @@ static int bin_place_impl(const uint64_t *depth_key, const int32_t *rect, const 
         VEGS_CHECK_LAUNCH();
         // 3. placement, one warp per chunk
         if (n_tiles <= 4096)
-            place_kernel<8><<<n_chunks, 32 * 8, sizeof(uint32_t) * n_tiles, s>>>(ids, (const int4 *)rect, n_kept, C,
+            place_kernel<8><<<n_chunks, 32 * 8, sizeof(uint32_t) * n_tiles, s>>>(ids, bin_rect, n_kept, C,
                                                                                tiles_x, tiles_y, counts, sorted_gauss,
                                                                                n_kept_dev);
         else
-            place_kernel<4><<<n_chunks, 32 * 4, sizeof(uint32_t) * n_tiles, s>>>(ids, (const int4 *)rect, n_kept, C,
+            place_kernel<4><<<n_chunks, 32 * 4, sizeof(uint32_t) * n_tiles, s>>>(ids, bin_rect, n_kept, C,
                                                                                tiles_x, tiles_y, counts, sorted_gauss,
                                                                                n_kept_dev);
         VEGS_CHECK_LAUNCH();
-        if ((inst_pid || order) && !counts_dev) {
+        if ((inst_pid || order) && !counts_dev && !cull_record) {
             placed_extras_kernel<<<(int)((n_inst + 255) / 256), 256, 0, s>>>(
                 sorted_gauss, (const int4 *)rect, offsets, kept_idx, tile_end, n_inst, n_tiles, tiles_x, inst_pid,
                 order);
@@ -672,9 +713,10 @@ extern "C" int vegs_bin_sort(const uint32_t *tiles, const uint64_t *depth_key, c
                              const int64_t *offsets, const int64_t *kept_idx, int64_t n, int64_t n_kept,
                              int64_t n_inst, int32_t width, int32_t height, int32_t tile_size,
                              uint32_t *sorted_gauss, uint32_t *inst_pid, int64_t *order,
-                             int32_t *tile_start, int32_t *tile_end, int32_t *tile_order, void *ws,
-                             size_t *ws_bytes, void *stream) {
+                             int32_t *tile_start, int32_t *tile_end, int32_t *tile_order,
+                             const float *cull_record, int32_t n_channels, void *ws, size_t *ws_bytes, void *stream) {
     if (!ws_bytes || tile_size != kTile || width < 1 || height < 1) return VEGS_ERR_ARG;
+    if (cull_record && ((n_channels != 3 && n_channels != 11) || inst_pid || order)) return VEGS_ERR_ARG;
     // instance positions are int32 (tile ranges, out_last): at most 2^31 - 1 instances per view
     if (n_inst > (int64_t)INT32_MAX || n >= (int64_t(1) << 32)) return VEGS_ERR_ARG;
     if (ws && (n > 0) && (!tiles || !depth_key || !rect || !offsets || !kept_idx)) return VEGS_ERR_ARG;
@@ -686,7 +728,8 @@ extern "C" int vegs_bin_sort(const uint32_t *tiles, const uint64_t *depth_key, c
     const bool force_radix = radix_env && radix_env[0] && radix_env[0] != '0';
     if ((tiles_x + 1) * (tiles_y + 1) <= kMaxPlaceTiles && !force_radix)
         return bin_place_impl(depth_key, rect, offsets, kept_idx, n, n_kept, n_inst, tiles_x, tiles_y, sorted_gauss,
-                              inst_pid, order, tile_start, tile_end, tile_order, ws, ws_bytes, s);
+                              inst_pid, order, tile_start, tile_end, tile_order, ws, ws_bytes, s, nullptr,
+                              cull_record, cull_record ? rec_stride(n_channels) : 0);
     if (n_tiles <= 65536)
         return bin_sort_impl<uint16_t>(tiles, depth_key, rect, offsets, kept_idx, n, n_kept, n_inst, tiles_x,
                                        n_tiles, sorted_gauss, inst_pid, order, tile_start, tile_end, tile_order, ws,
@@ -713,9 +756,11 @@ extern "C" int vegs_bin_count_dev(uint32_t *tiles, int64_t n, int64_t *offsets, 
 extern "C" int vegs_bin_sort_dev(const uint64_t *depth_key, const int32_t *rect, const int64_t *offsets,
                                  const int64_t *kept_idx, int64_t n, const int64_t *counts, int64_t kept_capacity,
                                  int32_t width, int32_t height, int32_t tile_size, uint32_t *sorted_gauss,
-                                 int32_t *tile_start, int32_t *tile_end, int32_t *tile_order, void *ws,
-                                 size_t *ws_bytes, void *stream) {
+                                 int32_t *tile_start, int32_t *tile_end, int32_t *tile_order,
+                                 const float *cull_record, int32_t n_channels, void *ws, size_t *ws_bytes,
+                                 void *stream) {
     if (!ws_bytes || tile_size != kTile || width < 1 || height < 1 || !counts) return VEGS_ERR_ARG;
+    if (cull_record && n_channels != 3 && n_channels != 11) return VEGS_ERR_ARG;
     if (n >= (int64_t(1) << 31)) return VEGS_ERR_ARG;
     const int tiles_x = (width + kTile - 1) / kTile, tiles_y = (height + kTile - 1) / kTile;
     if ((tiles_x + 1) * (tiles_y + 1) > kMaxPlaceTiles) return VEGS_ERR_ARG;  // radix path needs host counts
@@ -723,5 +768,6 @@ extern "C" int vegs_bin_sort_dev(const uint64_t *depth_key, const int32_t *rect,
     if (ws && (!tile_start || !tile_end || !sorted_gauss)) return VEGS_ERR_ARG;
     const int64_t kc = kept_capacity < n ? kept_capacity : n;
     return bin_place_impl(depth_key, rect, offsets, kept_idx, n, kc, 1, tiles_x, tiles_y, sorted_gauss, nullptr,
-                          nullptr, tile_start, tile_end, tile_order, ws, ws_bytes, (cudaStream_t)stream, counts);
+                          nullptr, tile_start, tile_end, tile_order, ws, ws_bytes, (cudaStream_t)stream, counts,
+                          cull_record, cull_record ? rec_stride(n_channels) : 0);
 }

@@ -235,7 +235,7 @@ class Rasterizer:
     may outlive later renders)."""
 
     def __init__(self, settings: RasterSettings = DEFAULT_SETTINGS, n_channels: int = 3,
-                 store_f64: bool = False, pooled: bool = True, fast_t: bool = False):
+                 store_f64: bool = False, pooled: bool = True, fast_t: bool = False, cull: bool = False):
         if n_channels not in (3, 11):
             raise ValueError("n_channels must be 3 (rgb) or 11 (rgb + aux planes)")
         self.device = require_cuda()
@@ -253,6 +253,8 @@ class Rasterizer:
         # float32 blends: carry T in float32 with exact decisions (vegs_composite_forward_fast)
         # instead of the float64 chain that reproduces the reference's T bit for bit
         self.fast_t = fast_t
+        # cull=True (training and render pipelines): bin on the tight ellipse boxes (_culls)
+        self.cull = cull
         # device-count binning (set by the Trainer): an int64[2] step state shared by the
         # views of a step and the instance capacity of this rasteriser's pooled buffers
         self.device_counts: torch.Tensor | None = None
@@ -264,6 +266,12 @@ class Rasterizer:
         """Counting placement (<= 12288 tiles, VEGS_BIN_RADIX unset) -- the C library's rule."""
         tx, ty = (width + TILE - 1) // TILE, (height + TILE - 1) // TILE
         return (tx + 1) * (ty + 1) <= 12288 and os.environ.get("VEGS_BIN_RADIX", "")[:1] in ("", "0")
+
+    def _culls(self) -> bool:
+        """Culled binning (tight ellipse boxes, float32 tables): tile lists hold only the
+        instances that can blend in their tile.  Same images and gradients; out_last and the
+        tile ranges then index the shorter lists, so the reference-shaped API never culls."""
+        return self.cull and not self.store_f64
 
     def _run(self, name: str, *args) -> None:
         if self.timer is not None:
@@ -373,11 +381,12 @@ class Rasterizer:
             n_kept, n_inst = int(self.kept_cap), int(self.inst_cap)  # capacities (the counts stay on the device)
             sorted_gauss = A.get("sorted_gauss", n_inst, torch.int32)
             args = (_p(depth_key), _p(rect), _p(offsets), _p(kept_idx), n, _p(pend["counts"]), int(self.kept_cap),
-                    width, height, TILE, _p(sorted_gauss), _p(tile_start), _p(tile_end), _p(tile_order))
+                    width, height, TILE, _p(sorted_gauss), _p(tile_start), _p(tile_end), _p(tile_order),
+                    _p(record) if self._culls() else None, self.n_ch)
             wsz = _lib.size_query("vegs_bin_sort_dev", *args, tail=(s,))
             ws = A.get("ws_sort", wsz, torch.uint8)
             self._run("vegs_bin_sort_dev", *args, _p(ws), ctypes.byref(ctypes.c_size_t(wsz)), s)
-            self.launches += 2  # the capacity check of vegs_bin_count_dev
+            self.launches += 2 + self._culls()  # the capacity check of vegs_bin_count_dev (+ the binning rects)
         else:
             pend["event"].synchronize()
             n_kept, n_inst = (int(x) for x in pend["host"].tolist())
@@ -385,11 +394,15 @@ class Rasterizer:
             sorted_gauss = A.get("sorted_gauss", n_inst, torch.int32)
             inst_pid = A.get("inst_pid", n_inst, torch.int32) if want_order else None
             order = A.get("order", n_inst, torch.int64) if want_order else None
+            cull = self._culls() and not want_order and self._placement(width, height)
             args = (_p(tiles), _p(depth_key), _p(rect), _p(offsets), _p(kept_idx), n, n_kept, n_inst, width, height,
-                    TILE, _p(sorted_gauss), _p(inst_pid), _p(order), _p(tile_start), _p(tile_end), _p(tile_order))
+                    TILE, _p(sorted_gauss), _p(inst_pid), _p(order), _p(tile_start), _p(tile_end), _p(tile_order),
+                    _p(record) if cull else None, self.n_ch)
             wsz = _lib.size_query("vegs_bin_sort", *args, tail=(s,))
             ws = A.get("ws_sort", wsz, torch.uint8)
             self._run("vegs_bin_sort", *args, _p(ws), ctypes.byref(ctypes.c_size_t(wsz)), s)
+            if cull:
+                self.launches += 1  # the binning rects
             if not self._placement(width, height):
                 self.launches += 1  # radix path
             elif want_order:
@@ -561,11 +574,12 @@ class RenderPipeline:
     Output frames are only valid until the lane that produced them is reused."""
 
     def __init__(self, settings: RasterSettings = DEFAULT_SETTINGS, n_channels: int = 3, lanes: int = 4,
-                 fast_t: bool = False):
+                 fast_t: bool = False, cull: bool = True):
         dev = self.device = require_cuda()
         main = torch.cuda.current_stream(dev)
         self.lanes = [(main if i == 0 else torch.cuda.Stream(dev),
-                       Rasterizer(settings, n_channels, pooled=True, fast_t=fast_t)) for i in range(max(1, lanes))]
+                       Rasterizer(settings, n_channels, pooled=True, fast_t=fast_t, cull=cull))
+                      for i in range(max(1, lanes))]
         for _, rz in self.lanes:
             rz.contrib_counts = False  # images only
 

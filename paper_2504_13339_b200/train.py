@@ -169,7 +169,8 @@ class _Lane:
         from .device import LossKernel
 
         self.stream = stream
-        self.rz = Rasterizer(tr.settings, 11 if tr.with_aux else 3, store_f64=False, pooled=True, fast_t=tr.fast_t)
+        self.rz = Rasterizer(tr.settings, 11 if tr.with_aux else 3, store_f64=False, pooled=True, fast_t=tr.fast_t,
+                             cull=tr.cull)
         self.rz.contrib_counts = False  # nobody reads them in training
         self.loss = LossKernel(tr.device)
         self.loss_launches = 0
@@ -197,8 +198,11 @@ class Trainer:
     def __init__(self, gs: GaussianSet, config: TrainConfig, settings: RasterSettings = DEFAULT_SETTINGS,
                  background=(1.0, 1.0, 1.0), l1_weight: float | None = None, group=None, with_aux: bool = False,
                  lanes: int = 4, fast_t: bool = False, graphs: bool = False, grad_payload: str = "f64",
-                 grad_buckets: int = 4):
+                 grad_buckets: int = 4, cull: bool = True):
         self.device = require_cuda()
+        # cull: bin each view on the tight ellipse boxes (Rasterizer._culls): shorter tile lists,
+        # the same images, losses and gradients
+        self.cull = cull
         # fast_t: the forward carries T in float32 with every skip / clamp / termination
         # decision exact (vegs_composite_forward_fast).  Default: the float64 chain, which
         # also reproduces T bit for bit and measured as fast (A/B)

@@ -17,6 +17,7 @@ from paper_2504_13339_b200.device import DeviceTF, Rasterizer  # noqa: E402
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--config", choices=("c2", "c3"), default="c3")
+    ap.add_argument("--no-cull", action="store_true", help="the reference's tile lists (default: culled, as the sweep)")
     args = ap.parse_args()
     if args.config == "c3":
         gs = scenes.blob_gaussians(3_000_000, seed=1)
@@ -26,7 +27,7 @@ def main():
         gs, _, tf_h, cams = scenes.config_scene("c2")
         cam, tf = cams[0], DeviceTF(tf_h)
     params = torch.from_numpy(gs.pack()).cuda()
-    rz = Rasterizer()
+    rz = Rasterizer(cull=not args.no_cull)
     rz.contrib_counts = False
     for _ in range(2):
         rz.forward(params, len(gs), tf, cam)
@@ -35,7 +36,8 @@ def main():
     fr = rz.forward(params, len(gs), tf, cam)
     torch.cuda.synchronize()
     torch.cuda.profiler.stop()
-    print(f"profiled one {args.config} render: {fr.n_kept} kept splats, {fr.n_inst} instances")
+    print(f"profiled one {args.config} render: {fr.n_kept} kept splats, {fr.n_inst} instances "
+          f"({int(fr.tile_end[-1])} tile-list entries)")
 
 
 if __name__ == "__main__":

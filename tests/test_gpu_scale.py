@@ -132,18 +132,35 @@ def test_c3_frame_through_render_pipeline_vs_reference():
     def keep(i, fr):
         got[i] = (fr.out_img.view(-1, 3).clone(), fr.out_t.clone(), fr.out_last.clone())
 
+    def keep_ids(i, fr):  # culled lists: the Gaussian behind each last-contributor position
+        last = fr.out_last.long()
+        gid = torch.where(last >= 0, fr.sorted_gauss[last.clamp(min=0)].long(), torch.full_like(last, -1))
+        got[i] = (fr.out_img.view(-1, 3).clone(), fr.out_t.clone(), gid)
+
     pix = d["pix"]
-    for fast in (False, True):  # the float64 chain (default) and the fast-T forward
-        got.clear()
-        pipe = RenderPipeline(lanes=3, fast_t=fast)
-        pipe.render(params, len(gs), [(cam, other), (cam, dtf), (cam, other), (cam, dtf)], on_frame=keep)
-        torch.cuda.synchronize()
-        for i in (1, 3):
-            rgb, t, last = (x.cpu().numpy() for x in got[i])
-            assert np.array_equal(digest(last.astype(np.int64), np.int64), d["out_last_sha"]), (fast, i)
-            assert img_close(t[pix], d["pix_t"]) and img_close(rgb[pix], d["pix_rgb"]), (fast, i)
-            if not fast:
-                assert np.array_equal(digest(t, np.float32), d["out_t_sha"]), i
+    last_gid = None
+    for cull in (False, True):  # the reference's tile lists, then the culled ones the sweep uses
+        for fast in (False, True):  # the float64 chain (default) and the fast-T forward
+            got.clear()
+            pipe = RenderPipeline(lanes=3, fast_t=fast, cull=cull)
+            pipe.render(params, len(gs), [(cam, other), (cam, dtf), (cam, other), (cam, dtf)],
+                        on_frame=keep_ids if cull else keep)
+            torch.cuda.synchronize()
+            for i in (1, 3):
+                rgb, t, last = (x.cpu().numpy() for x in got[i])
+                if cull:  # the same last contributors, at other list positions
+                    assert np.array_equal(last, last_gid), (fast, i)
+                else:
+                    assert np.array_equal(digest(last.astype(np.int64), np.int64), d["out_last_sha"]), (fast, i)
+                assert img_close(t[pix], d["pix_t"]) and img_close(rgb[pix], d["pix_rgb"]), (cull, fast, i)
+                if not fast:
+                    assert np.array_equal(digest(t, np.float32), d["out_t_sha"]), (cull, i)
+        if not cull:
+            rz = Rasterizer(pooled=False)
+            fr = rz.forward(params, len(gs), dtf, cam)
+            lf = fr.out_last.long()
+            last_gid = torch.where(lf >= 0, fr.sorted_gauss[lf.clamp(min=0)].long(), torch.full_like(lf, -1))
+            last_gid = last_gid.cpu().numpy()
 
 
 @pytest.mark.parametrize("lanes", [1, 2, 3, 4])
@@ -157,7 +174,7 @@ def test_render_pipeline_frames_equal_single_stream(lanes):
     tfs = [DeviceTF(scenes.random_tf(1000 + k)) for k in range(3)]
     items = [(cams[i % len(cams)], tfs[i % len(tfs)]) for i in range(7)]
     ref = []
-    rz = Rasterizer(pooled=False)  # the pipeline's forward, single stream
+    rz = Rasterizer(pooled=False, cull=True)  # the pipeline's forward (culled binning), single stream
     for cam, tf in items:
         fr = rz.forward(params, len(gs), tf, cam)
         ref.append((fr.out_img.clone(), fr.out_t.clone(), fr.out_last.clone()))
@@ -175,6 +192,60 @@ def test_render_pipeline_frames_equal_single_stream(lanes):
         for i, (img, t, last) in enumerate(ref):
             gi, gt, gl = got[i]
             assert torch.equal(gi, img) and torch.equal(gt, t) and torch.equal(gl, last), (lanes, i)
+
+
+def _last_gauss(fr):
+    last = fr.out_last.long()
+    return torch.where(last >= 0, fr.sorted_gauss[last.clamp(min=0)].long(), torch.full_like(last, -1))
+
+
+@pytest.mark.parametrize("n_ch", [3, 11])
+def test_culled_binning_gives_identical_frames_and_gradients(n_ch):
+    """Binning on the tight ellipse boxes (the training / render pipelines) drops about a
+    quarter of the tile instances -- the ones that cannot blend in their tile -- and leaves
+    everything else bitwise unchanged: image, T, contributor counts, the last contributor
+    (as a Gaussian id: positions index the shorter lists), and the whole backward
+    (gradients, view-space norms, visibility, densify statistics)."""
+    if n_ch == 3:
+        gs, _, tf_h, cams = scenes.config_scene("c2")  # full config 2: 1M Gaussians at 1024^2
+        cam = cams[0]
+    else:
+        gs = scenes.random_gaussians(20_000, seed=4)
+        tf_h = scenes.random_tf(2, 4)
+        cam = scenes.orbit_cameras(1, 3, 200, 150)[0]
+    dtf = DeviceTF(tf_h)
+    params = torch.from_numpy(gs.pack()).cuda()
+    out = {}
+    for cull in (False, True):
+        rz = Rasterizer(n_channels=n_ch, pooled=False, cull=cull)
+        fr = rz.forward(params, len(gs), dtf, cam)
+        g = torch.Generator(device="cuda").manual_seed(7)
+        d_img = torch.rand(fr.out_img.shape, device="cuda", generator=g) - 0.5
+        d_alpha = torch.rand(fr.out_t.shape, device="cuda", generator=g) - 0.5
+        vs = torch.zeros(len(gs), dtype=torch.float64, device="cuda")
+        vis = torch.zeros(len(gs), dtype=torch.uint8, device="cuda")
+        dst = torch.zeros(5 * len(gs), dtype=torch.float64, device="cuda")
+        grads = rz.backward(fr, d_img, d_alpha, viewspace_norm=vs, visible=vis, densify_stats=dst)
+        n_listed = int((fr.tile_end - fr.tile_start).sum())
+        out[cull] = (fr.out_img, fr.out_t, fr.n_contrib, _last_gauss(fr), grads, vs, vis, dst, n_listed, fr.n_inst)
+    full, cut = out[False], out[True]
+    for k in range(8):
+        assert torch.equal(full[k], cut[k]), k
+    assert full[8] == full[9] and cut[9] == full[9]  # the reference lists hold every instance
+    assert cut[8] < full[8] and (n_ch == 11 or cut[8] < 0.85 * full[8])
+
+
+def test_culled_trainer_steps_equal_unculled():
+    """Trainer steps (device counts, CUDA graphs) with culled binning are bitwise the
+    reference-list steps."""
+    learned, dtf, cams, targets = _train_scene(4)
+    views = [View(c, dtf, t) for c, t in zip(cams, targets)]
+    res = []
+    for cull in (False, True):
+        tr = Trainer(learned, TrainConfig(iterations=100), graphs=True, cull=cull)
+        losses = [float(tr.step(views, iteration=it).item()) for it in (1, 2, 3)]
+        res.append((losses, tr.params.clone()))
+    assert res[0][0] == res[1][0] and torch.equal(res[0][1], res[1][1])
 
 
 def _train_scene(n_views, w=64, h=64):

@@ -51,7 +51,7 @@ def test_cub_workspace_queries():
     n = 1000
     b = _lib.size_query("vegs_bin_count", None, n, None, None, None, tail=(None,))
     assert b > 8 * n
-    args = (None, None, None, None, None, n, n, 20 * n, 512, 512, 16, None, None, None, None, None, None)
+    args = (None, None, None, None, None, n, n, 20 * n, 512, 512, 16, None, None, None, None, None, None, None, 3)
     b2 = _lib.size_query("vegs_bin_sort", *args, tail=(None,))
     assert b2 > 4 * 4 * n
 
@@ -59,14 +59,14 @@ def test_cub_workspace_queries():
 def test_bad_arguments_are_rejected_not_thrown():
     with pytest.raises(ValueError):
         _lib.call("vegs_bin_sort", None, None, None, None, None, 10, 10, 10, 64, 64, 8, None, None, None,
-                  None, None, None, None, ctypes.byref(ctypes.c_size_t(0)), None)
+                  None, None, None, None, 3, None, ctypes.byref(ctypes.c_size_t(0)), None)
     with pytest.raises(ValueError):
         _lib.call("vegs_composite_forward", None, None, None, None, None, 3, 0, None, 64, 64, 0.99, 1e-4,
                   None, None, None, None, None, None)
     # more instances than int32 positions can address: refused before any CUDA call
     with pytest.raises(ValueError):
         _lib.size_query("vegs_bin_sort", None, None, None, None, None, 1000, 1000, 2**31, 512, 512, 16, None,
-                        None, None, None, None, None, tail=(None,))
+                        None, None, None, None, None, None, 3, tail=(None,))
 
 
 def test_parameter_pack_roundtrip():
