@@ -1,0 +1,53 @@
+"""Binning primitives at scale: vegs_bin_count's scan of the (kept, tiles) counters against
+numpy's cumulative sums, and the compositing launch order (heaviest tiles first, ties in
+tile order) against numpy's stable argsort."""
+
+import ctypes
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("needs CUDA", allow_module_level=True)
+
+from paper_2504_13339_b200 import _lib  # noqa: E402
+
+
+@pytest.mark.parametrize("n", [1, 2047, 2048, 2049, 300_001, 3_000_000])
+def test_bin_count_scan_matches_numpy(n):
+    """vegs_bin_count: offsets, kept indices and totals against numpy's cumulative sums."""
+    rng = np.random.default_rng(n)
+    tiles = rng.integers(0, 40, n).astype(np.uint32)
+    tiles[rng.random(n) < 0.3] = 0  # culled splats
+    t = torch.from_numpy(tiles.view(np.int32)).cuda()
+    offs = torch.empty(n + 1, dtype=torch.int64, device="cuda")
+    kept = torch.empty(n + 1, dtype=torch.int64, device="cuda")
+    counts = torch.empty(2, dtype=torch.int64, device="cuda")
+    p = lambda x: ctypes.c_void_p(x.data_ptr())  # noqa: E731
+    nb = _lib.size_query("vegs_bin_count", p(t), n, p(offs), p(kept), p(counts), tail=(None,))
+    ws = torch.empty(nb, dtype=torch.uint8, device="cuda")
+    _lib.call("vegs_bin_count", p(t), n, p(offs), p(kept), p(counts), p(ws), ctypes.byref(ctypes.c_size_t(nb)), None)
+    torch.cuda.synchronize()
+    ref_off = np.concatenate([[0], np.cumsum(tiles.astype(np.int64))])
+    ref_kept = np.concatenate([[0], np.cumsum((tiles > 0).astype(np.int64))])
+    assert np.array_equal(offs.cpu().numpy(), ref_off) and np.array_equal(kept.cpu().numpy(), ref_kept)
+    assert counts.cpu().tolist() == [int(ref_kept[-1]), int(ref_off[-1])]
+
+
+@pytest.mark.parametrize("wh", [(1024, 1024), (1920, 1080), (200, 120)])
+def test_tile_launch_order_is_heaviest_first_stable(wh):
+    """The compositing launch order: tiles by decreasing instance count, ties in tile
+    order -- numpy's stable argsort of 0xffff - min(count, 0xffff)."""
+    from paper_2504_13339_b200 import scenes
+    from paper_2504_13339_b200.device import DeviceTF, Rasterizer
+
+    gs = scenes.blob_gaussians(200_000, seed=2)
+    cam = scenes.orbit_cameras(1, 5, *wh)[0]
+    rz = Rasterizer(pooled=False, cull=True)
+    fr = rz.forward(torch.from_numpy(gs.pack()).cuda(), len(gs), DeviceTF(scenes.random_tf(7)), cam)
+    c = (fr.tile_end - fr.tile_start).cpu().numpy().astype(np.int64)
+    key = 0xFFFF - np.minimum(c, 0xFFFF)
+    assert np.array_equal(fr.tile_order.cpu().numpy(), np.argsort(key, kind="stable"))
