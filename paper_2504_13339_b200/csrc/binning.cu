@@ -313,12 +313,12 @@ __global__ void chunk_offsets_kernel(uint32_t *counts, const uint32_t *gbase, co
     if (grp == 0) tile_end[t] = tile_start[t] + (int32_t)total[t];
     uint32_t run = (uint32_t)tile_start[t] + gbase[i];
     const int c0 = grp * G, c1 = (grp + 1) * G < n_chunks ? (grp + 1) * G : n_chunks;
-    for (int cb = c0; cb < c1; cb += 8) {  // 8 loads in flight, then 8 stores
-        uint32_t v[8];
+    for (int cb = c0; cb < c1; cb += 16) {  // 16 loads in flight, then 16 stores
+        uint32_t v[16];
 #pragma unroll
-        for (int q = 0; q < 8; ++q) v[q] = cb + q < c1 ? counts[(size_t)(cb + q) * n_tiles + t] : 0u;
+        for (int q = 0; q < 16; ++q) v[q] = cb + q < c1 ? counts[(size_t)(cb + q) * n_tiles + t] : 0u;
 #pragma unroll
-        for (int q = 0; q < 8; ++q)
+        for (int q = 0; q < 16; ++q)
             if (cb + q < c1) {
                 counts[(size_t)(cb + q) * n_tiles + t] = run;
                 run += v[q];
@@ -340,10 +340,21 @@ __global__ void __launch_bounds__(32 * kBands) place_kernel(const uint32_t *ids,
     extern __shared__ uint32_t cursor[];
     const int n_tiles = tiles_x * tiles_y;
     const int c = blockIdx.x, lane = threadIdx.x & 31, band = threadIdx.x >> 5;
-    for (int t = threadIdx.x; t < n_tiles; t += blockDim.x) cursor[t] = first[(size_t)c * n_tiles + t];
-    __syncthreads();
-    const int band_lo = band * tiles_y / kBands, band_hi = (band + 1) * tiles_y / kBands - 1;  // tile rows
+    // the chunk's first slots straight into SMEM (LDGSTS, all in flight; 16-byte pieces when
+    // the rows are aligned): a load-then-store loop left every cursor a dependent round trip
     const int64_t lo = (int64_t)c * C, hi = lo + C < n_kept ? lo + C : n_kept;
+    if (lo >= hi) return;  // (device counts: chunks past the kept splats)
+    const uint32_t *src = first + (size_t)c * n_tiles;
+    const uint32_t cur0 = (uint32_t)__cvta_generic_to_shared(cursor);
+    if ((n_tiles & 3) == 0) {
+        for (int q = threadIdx.x; q < (n_tiles >> 2); q += blockDim.x)
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(cur0 + 16u * q), "l"(src + 4 * q));
+    } else {
+        for (int t = threadIdx.x; t < n_tiles; t += blockDim.x)
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(cur0 + 4u * t), "l"(src + t));
+    }
+    asm volatile("cp.async.commit_group;\n" ::);
+    const int band_lo = band * tiles_y / kBands, band_hi = (band + 1) * tiles_y / kBands - 1;  // tile rows
     // lane k holds splat r0 + k of the current group of 32; the next group's ids and rects
     // are fetched while this one is placed
     auto fetch = [&](int64_t r0, uint32_t &g, int4 &q) {
@@ -356,7 +367,9 @@ __global__ void __launch_bounds__(32 * kBands) place_kernel(const uint32_t *ids,
     };
     uint32_t g_n;
     int4 q_n;
-    fetch(lo, g_n, q_n);
+    fetch(lo, g_n, q_n);  // overlaps the cursor copy
+    asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+    __syncthreads();
     for (int64_t r0 = lo; r0 < hi; r0 += 32) {
         const uint32_t g = g_n;
         const int4 q = q_n;
