@@ -166,7 +166,9 @@ int vegs_bin_sort(const uint32_t *tiles, const uint64_t *depth_key, const int32_
  * caller grows its capacities and redoes the step; the trainer's Adam skips on it).  tiles
  * is therefore read-write.  Same ws as vegs_bin_count.
  * vegs_bin_sort_dev = vegs_bin_sort's counting placement with n_kept read from counts
- * (device); launches and the workspace are sized for kept_capacity kept splats.  Views
+ * (device); launches and the workspace are sized for kept_capacity kept splats and
+ * inst_capacity instances (the sorted_gauss capacity, which also bounds the placement's
+ * per-block lists).  Views
  * above 12288 tiles need the radix path and host counts: VEGS_ERR_ARG.  cull_record as
  * in vegs_bin_sort. */
 int vegs_bin_count_dev(uint32_t *tiles, int64_t n, int64_t *offsets, int64_t *kept_idx, int64_t *counts,
@@ -174,6 +176,7 @@ int vegs_bin_count_dev(uint32_t *tiles, int64_t n, int64_t *offsets, int64_t *ke
                        void *ws, size_t *ws_bytes, void *stream);
 int vegs_bin_sort_dev(const uint64_t *depth_key, const int32_t *rect, const int64_t *offsets,
                       const int64_t *kept_idx, int64_t n, const int64_t *counts, int64_t kept_capacity,
+                      int64_t inst_capacity,
                       int32_t width, int32_t height, int32_t tile_size, uint32_t *sorted_gauss,
                       int32_t *tile_start, int32_t *tile_end, int32_t *tile_order, const float *cull_record,
                       int32_t n_channels, void *ws, size_t *ws_bytes, void *stream);

@@ -80,8 +80,8 @@ _SIGS = {
     "vegs_grad_pack": [P, P, P, P, P, c_int64, c_int32, c_int32, P],
     "vegs_adam_step_range": [P, P, P, P, P, c_int64, c_int32, c_int32, P, P, P, P],
     "vegs_bin_count_dev": [P, c_int64, P, P, P, c_int64, c_int64, P, P, P, POINTER(c_size_t), P],
-    "vegs_bin_sort_dev": [P, P, P, P, c_int64, P, c_int64, c_int32, c_int32, c_int32, P, P, P, P, P, c_int32,
-                          P, POINTER(c_size_t), P],
+    "vegs_bin_sort_dev": [P, P, P, P, c_int64, P, c_int64, c_int64, c_int32, c_int32, c_int32, P, P, P, P, P,
+                          c_int32, P, POINTER(c_size_t), P],
 }
 
 _lib = None

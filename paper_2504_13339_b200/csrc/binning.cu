@@ -249,7 +249,8 @@ __global__ void bin_rect_kernel(const float *record, int rs, const int4 *rect, i
 // rank) = depth rank order: exactly np.lexsort((depth, tile)), as the radix path.
 
 __global__ void chunk_count_kernel(const uint32_t *ids, const int4 *rect, int64_t n_kept, int C, int tiles_x,
-                                   int tiles_y, uint32_t *counts, const int64_t *n_kept_dev = nullptr) {
+                                   int tiles_y, uint32_t *counts, const int64_t *n_kept_dev = nullptr,
+                                   int shift = 4) {  // cells of 2^shift pixels (tiles, or 4x4-tile blocks)
     if (n_kept_dev) n_kept = *n_kept_dev;  // device-count binning: chunks past the kept splats count zero
     extern __shared__ int diff[];  // (tiles_y + 1) x (tiles_x + 1)
     const int c = blockIdx.x, W1 = tiles_x + 1, n_diff = (tiles_y + 1) * W1, n_tiles = tiles_x * tiles_y;
@@ -259,7 +260,7 @@ __global__ void chunk_count_kernel(const uint32_t *ids, const int4 *rect, int64_
     for (int64_t r = lo + threadIdx.x; r < hi; r += blockDim.x) {
         const int4 q = __ldg(rect + ids[r]);
         if (q.y <= q.x || q.w <= q.z) continue;  // a culled-empty binning rect
-        const int x0 = q.x / kTile, x1 = (q.y - 1) / kTile + 1, y0 = q.z / kTile, y1 = (q.w - 1) / kTile + 1;
+        const int x0 = q.x >> shift, x1 = ((q.y - 1) >> shift) + 1, y0 = q.z >> shift, y1 = ((q.w - 1) >> shift) + 1;
         atomicAdd(&diff[y0 * W1 + x0], 1);
         atomicAdd(&diff[y0 * W1 + x1], -1);
         atomicAdd(&diff[y1 * W1 + x0], -1);
@@ -335,7 +336,8 @@ __global__ void chunk_offsets_kernel(uint32_t *counts, const uint32_t *gbase, co
 template <int kBands>
 __global__ void __launch_bounds__(32 * kBands) place_kernel(const uint32_t *ids, const int4 *rect, int64_t n_kept,
                                                             int C, int tiles_x, int tiles_y, const uint32_t *first,
-                                                            uint32_t *sorted_gauss, const int64_t *n_kept_dev = nullptr) {
+                                                            uint32_t *sorted_gauss, const int64_t *n_kept_dev = nullptr,
+                                                            int shift = 4) {
     if (n_kept_dev) n_kept = *n_kept_dev;
     extern __shared__ uint32_t cursor[];
     const int n_tiles = tiles_x * tiles_y;
@@ -374,8 +376,8 @@ __global__ void __launch_bounds__(32 * kBands) place_kernel(const uint32_t *ids,
         const uint32_t g = g_n;
         const int4 q = q_n;
         if (r0 + 32 < hi) fetch(r0 + 32, g_n, q_n);
-        const int x0 = q.x / kTile, nx = (q.y - 1) / kTile - x0 + 1;
-        const int ys = max(q.z / kTile, band_lo), ye = min((q.w - 1) / kTile, band_hi);
+        const int x0 = q.x >> shift, nx = ((q.y - 1) >> shift) - x0 + 1;
+        const int ys = max(q.z >> shift, band_lo), ye = min((q.w - 1) >> shift, band_hi);
         const int cnt = r0 + lane < hi && ys <= ye && q.x < q.y ? nx * (ye - ys + 1) : 0;
         const float inx = 1.0f / (float)nx;
         unsigned todo = __ballot_sync(0xffffffffu, cnt > 0);  // splats of the group touching this band
@@ -399,6 +401,145 @@ __global__ void __launch_bounds__(32 * kBands) place_kernel(const uint32_t *ids,
             }
             __syncwarp();
         }
+    }
+}
+
+// ---- two-level placement ---------------------------------------------------------------
+// Level 1 runs the counting placement above on a grid of 4x4-tile blocks: per block, the ids
+// of the splats whose binning rect touches it, in depth order (about 1.3 entries per kept
+// splat at c2 / c3 against ~25 tile instances).  Level 2 runs one CTA per block over that
+// list in batches of 256 splats: each thread takes one splat and the 16-bit mask of the
+// block's tiles its rect covers; per tile, a ballot ranks the warp's splats in list (= depth)
+// order and the warps' counts are scanned in SMEM, so every tile's entries of a batch are
+// written as one contiguous run -- one coalesced store per tile and warp instead of one
+// scattered 4-byte store per instance (the single-level placement was bound by those L2
+// write requests: 0.44 ms of a 1080p frame).  Result identical to the single level:
+// per tile, the splats in depth order.
+constexpr int kBlk = 4;  // tiles per block side
+
+__device__ __forceinline__ uint32_t block_tile_mask(int4 q, int bx0, int by0, int tiles_x, int tiles_y) {
+    if (q.y <= q.x || q.w <= q.z) return 0u;
+    const int x0 = max(q.x >> 4, bx0), x1 = min((q.y - 1) >> 4, min(bx0 + kBlk - 1, tiles_x - 1));
+    const int y0 = max(q.z >> 4, by0), y1 = min((q.w - 1) >> 4, min(by0 + kBlk - 1, tiles_y - 1));
+    if (x0 > x1 || y0 > y1) return 0u;
+    const uint32_t row = ((1u << (x1 - x0 + 1)) - 1u) << (x0 - bx0);
+    uint32_t m = 0;
+#pragma unroll
+    for (int y = 0; y < kBlk; ++y)
+        if (by0 + y >= y0 && by0 + y <= y1) m |= row << (kBlk * y);
+    return m;
+}
+
+// per tile: its instance count, from 2D difference arrays of the kept splats' binning rects:
+// each CTA accumulates its share of the splats in a private SMEM array (4 SMEM atomics per
+// splat), then adds that array into the global one (every address once per CTA: no hot spots)
+__global__ void __launch_bounds__(256) tile_diff_kernel(const uint32_t *ids, const int4 *rect, int64_t n_kept,
+                                                        int tiles_x, int tiles_y, int *diff,
+                                                        const int64_t *n_kept_dev) {
+    extern __shared__ int s_diff[];
+    if (n_kept_dev) n_kept = *n_kept_dev;
+    const int W1 = tiles_x + 1, n_diff = W1 * (tiles_y + 1);
+    for (int i = threadIdx.x; i < n_diff; i += blockDim.x) s_diff[i] = 0;
+    __syncthreads();
+    for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < n_kept; r += (int64_t)gridDim.x * blockDim.x) {
+        const int4 q = __ldg(rect + ids[r]);
+        if (q.y <= q.x || q.w <= q.z) continue;
+        const int x0 = q.x >> 4, x1 = ((q.y - 1) >> 4) + 1, y0 = q.z >> 4, y1 = ((q.w - 1) >> 4) + 1;
+        atomicAdd(&s_diff[y0 * W1 + x0], 1);
+        atomicAdd(&s_diff[y0 * W1 + x1], -1);
+        atomicAdd(&s_diff[y1 * W1 + x0], -1);
+        atomicAdd(&s_diff[y1 * W1 + x1], 1);
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < n_diff; i += blockDim.x)
+        if (s_diff[i]) atomicAdd(diff + i, s_diff[i]);
+}
+
+__global__ void __launch_bounds__(1024) tile_total_kernel(const int *diff, int tiles_x, int tiles_y,
+                                                          uint32_t *total) {
+    extern __shared__ int s_d[];  // the difference array, prefix-summed in SMEM
+    const int W1 = tiles_x + 1, n_diff = W1 * (tiles_y + 1);
+    for (int i = threadIdx.x; i < n_diff; i += blockDim.x) s_d[i] = diff[i];
+    __syncthreads();
+    for (int y = threadIdx.x; y < tiles_y; y += blockDim.x) {  // prefix along rows
+        int run = 0;
+        for (int x = 0; x < tiles_x; ++x) s_d[y * W1 + x] = (run += s_d[y * W1 + x]);
+    }
+    __syncthreads();
+    for (int x = threadIdx.x; x < tiles_x; x += blockDim.x) {  // prefix along columns
+        int run = 0;
+        for (int y = 0; y < tiles_y; ++y) total[y * tiles_x + x] = (uint32_t)(run += s_d[y * W1 + x]);
+    }
+}
+
+// level 2: the block's tiles filled run by run (the next batch's ids and rects are fetched
+// while one is placed); tile_end from the final cursors
+__global__ void __launch_bounds__(256) block_place_kernel(const uint32_t *coarse, const int32_t *blk_start,
+                                                          const int32_t *blk_end, const int4 *rect, int tiles_x,
+                                                          int tiles_y, int bx, const int32_t *tile_start,
+                                                          int32_t *tile_end, uint32_t *sorted_gauss) {
+    constexpr int NB = kBlk * kBlk, NW = 8, K = 2;  // K splats per thread per batch
+    __shared__ uint32_t s_cur[NB];      // next slot of each tile
+    __shared__ uint32_t s_wc[NW][NB];   // per-warp counts of the batch, then the warps' first slots
+    const int blk = blockIdx.x, bx0 = (blk % bx) * kBlk, by0 = (blk / bx) * kBlk;
+    const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+    const unsigned lt = (1u << lane) - 1u;
+    if (t < NB) {
+        const int tx = bx0 + t % kBlk, ty = by0 + t / kBlk;
+        s_cur[t] = tx < tiles_x && ty < tiles_y ? (uint32_t)tile_start[ty * tiles_x + tx] : 0u;
+    }
+    const int beg = blk_start[blk], end = blk_end[blk];
+    // batch layout: splat beg + i0 + k * 256 + t for k < K (each warp's splats stay in list order
+    // per k; the K sub-batches are ranked one after the other)
+    uint32_t g_n[K];
+    int4 q_n[K];
+    auto fetch = [&](int i0) {
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+            const int i = i0 + k * 256 + t;
+            g_n[k] = i < end ? coarse[i] : 0u;
+            q_n[k] = i < end ? __ldg(rect + g_n[k]) : make_int4(0, 0, 0, 0);
+        }
+    };
+    fetch(beg);
+    __syncthreads();
+    for (int i0 = beg; i0 < end; i0 += K * 256) {  // block-uniform trip count
+        uint32_t g[K], m[K];
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+            g[k] = g_n[k];
+            m[k] = block_tile_mask(q_n[k], bx0, by0, tiles_x, tiles_y);
+        }
+        if (i0 + K * 256 < end) fetch(i0 + K * 256);
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+            uint32_t bal[NB];
+#pragma unroll
+            for (int b = 0; b < NB; ++b) {
+                bal[b] = __ballot_sync(0xffffffffu, (m[k] >> b) & 1u);
+                if (lane == 0) s_wc[w][b] = __popc(bal[b]);
+            }
+            __syncthreads();
+            if (t < NB) {  // tile t: the warps' first slots in list order, then the cursor moves on
+                uint32_t run = s_cur[t];
+#pragma unroll
+                for (int j = 0; j < NW; ++j) {
+                    const uint32_t c = s_wc[j][t];
+                    s_wc[j][t] = run;
+                    run += c;
+                }
+                s_cur[t] = run;
+            }
+            __syncthreads();
+#pragma unroll
+            for (int b = 0; b < NB; ++b)
+                if ((m[k] >> b) & 1u) sorted_gauss[s_wc[w][b] + __popc(bal[b] & lt)] = g[k];
+            __syncthreads();  // s_wc is rewritten by the next sub-batch
+        }
+    }
+    if (t < NB) {
+        const int tx = bx0 + t % kBlk, ty = by0 + t / kBlk;
+        if (tx < tiles_x && ty < tiles_y) tile_end[ty * tiles_x + tx] = (int32_t)s_cur[t];
     }
 }
 
@@ -601,13 +742,28 @@ static int bin_place_impl(const uint64_t *depth_key, const int32_t *rect, const 
                           int tiles_y, uint32_t *sorted_gauss, uint32_t *inst_pid, int64_t *order,
                           int32_t *tile_start, int32_t *tile_end, int32_t *tile_order, void *ws, size_t *ws_bytes,
                           cudaStream_t s, const int64_t *counts_dev = nullptr, const float *cull_record = nullptr,
-                          int rs = 0) {
+                          int rs = 0, int64_t inst_capacity = 0) {
     // counts_dev (device-count binning): n_kept / n_inst live on the device; every launch is
     // sized for n kept splats and the kernels read the real count (no host sync)
     const int64_t *n_kept_dev = counts_dev;
     if (counts_dev) n_inst = 1;  // n_kept: the caller's kept capacity; n_inst only meets the zero test below
     const int64_t n_sort = counts_dev ? n_kept : n;  // keys sorted: all n, or the compacted kept capacity
     const int n_tiles = tiles_x * tiles_y;
+    // two-level placement (default; VEGS_PLACE_FLAT=1: the single level, for A/B and tests):
+    // level 1 over 4x4-tile blocks, level 2 block by block (see block_place_kernel)
+    // Two levels from 4096 tiles up: the single level's scattered 4-byte writes (20M per
+    // config-2 view, 48M per config-3 frame) throttle the other stream lanes' compositing,
+    // so although each level-2 kernel is latency-bound alone, the pipelined step gains 2%
+    // and the 1080p sweep 20%; small views (config 4, 2500 tiles) stay on one level, where
+    // the extra launches cost more.  VEGS_PLACE_FLAT=1 / =0 forces one or two
+    // levels (tests, A/B)
+    const char *flat_env = getenv("VEGS_PLACE_FLAT");
+    const bool two = flat_env && flat_env[0] ? flat_env[0] == '0' : n_tiles >= 4096;
+    const int bx = (tiles_x + kBlk - 1) / kBlk, by = (tiles_y + kBlk - 1) / kBlk, n_blk = bx * by;
+    const int cells_x = two ? bx : tiles_x, cells_y = two ? by : tiles_y, n_cells = cells_x * cells_y;
+    const int cell_shift = two ? 6 : 4;  // log2 of the level-1 cell size in pixels
+    // coarse list capacity: a (splat, block) entry implies >= 1 tile instance
+    const int64_t coarse_cap = two ? (counts_dev ? inst_capacity : n_inst) : 0;
 #ifndef VEGS_PLACE_CHUNKS
 #define VEGS_PLACE_CHUNKS 2048
 #endif
@@ -630,10 +786,16 @@ static int bin_place_impl(const uint64_t *depth_key, const int32_t *rect, const 
     size_t t_max = t_depth > t_scan ? t_depth : t_scan;
     t_max = t_max > t_tiles ? t_max : t_tiles;
     const size_t b_n = align_up(sizeof(uint32_t) * (n + 1)), b_t = align_up(sizeof(uint32_t) * n_tiles);
-    const size_t b_cnt = align_up(sizeof(uint32_t) * (size_t)n_chunks * n_tiles);
-    const size_t b_grp = align_up(sizeof(uint32_t) * (size_t)n_groups * n_tiles);
+    const size_t b_cnt = align_up(sizeof(uint32_t) * (size_t)n_chunks * n_cells);
+    size_t b_grp = align_up(sizeof(uint32_t) * (size_t)n_groups * n_cells);
+    if (two) {  // reused for the tile difference array
+        const size_t b_diff = align_up(sizeof(int) * (size_t)(tiles_x + 1) * (tiles_y + 1));
+        b_grp = b_grp > b_diff ? b_grp : b_diff;
+    }
+    const size_t b_blk = two ? 3 * align_up(sizeof(uint32_t) * n_blk) : 0;
+    const size_t b_coarse = align_up(sizeof(uint32_t) * (size_t)(coarse_cap > 0 ? coarse_cap : 1));
     const size_t b_rect = cull_record ? align_up(sizeof(int4) * n) : 0;
-    const size_t need = 4 * b_n + b_cnt + b_grp + 4 * b_t + align_up(t_max) + b_rect;
+    const size_t need = 4 * b_n + b_cnt + b_grp + 4 * b_t + align_up(t_max) + b_rect + b_blk + (two ? b_coarse : 0);
     if (!ws) {
         *ws_bytes = need;
         return VEGS_OK;
@@ -651,6 +813,15 @@ static int bin_place_impl(const uint64_t *depth_key, const int32_t *rect, const 
     uint32_t *tkey0 = (uint32_t *)w; w += b_t;
     uint32_t *tkey1 = (uint32_t *)w; w += b_t;
     int32_t *tval = (int32_t *)w; w += b_t;
+    uint32_t *ctotal = nullptr, *coarse = nullptr;
+    int32_t *cstart = nullptr, *cend = nullptr;
+    if (two) {
+        const size_t b1 = align_up(sizeof(uint32_t) * n_blk);
+        ctotal = (uint32_t *)w; w += b1;
+        cstart = (int32_t *)w; w += b1;
+        cend = (int32_t *)w; w += b1;
+        coarse = (uint32_t *)w; w += b_coarse;
+    }
     void *tmp = w;
     const size_t tb0 = align_up(t_max);
 
@@ -680,31 +851,52 @@ static int bin_place_impl(const uint64_t *depth_key, const int32_t *rect, const 
             VEGS_CHECK_LAUNCH();
             bin_rect = brect;
         }
-        // 2. per-chunk tile counts -> first slot of every chunk in every tile, tile ranges
-        const size_t diff_bytes = sizeof(int) * (size_t)(tiles_x + 1) * (tiles_y + 1);
-        chunk_count_kernel<<<n_chunks, 256, diff_bytes, s>>>(ids, bin_rect, n_kept, C, tiles_x, tiles_y, counts,
-                                                             n_kept_dev);
+        // 2. per-chunk cell counts -> first slot of every chunk in every cell, cell ranges
+        //    (cells: the tiles, or with two levels the 4x4-tile blocks)
+        const size_t diff_bytes = sizeof(int) * (size_t)(cells_x + 1) * (cells_y + 1);
+        uint32_t *ctot = two ? ctotal : total;
+        int32_t *c_start = two ? cstart : tile_start, *c_end = two ? cend : tile_end;
+        chunk_count_kernel<<<n_chunks, 256, diff_bytes, s>>>(ids, bin_rect, n_kept, C, cells_x, cells_y, counts,
+                                                             n_kept_dev, cell_shift);
         VEGS_CHECK_LAUNCH();
-        const int64_t ng = (int64_t)n_groups * n_tiles;
-        chunk_group_sum_kernel<<<(int)((ng + 255) / 256), 256, 0, s>>>(counts, n_chunks, n_tiles, G, gsum);
+        const int64_t ng = (int64_t)n_groups * n_cells;
+        chunk_group_sum_kernel<<<(int)((ng + 255) / 256), 256, 0, s>>>(counts, n_chunks, n_cells, G, gsum);
         VEGS_CHECK_LAUNCH();
-        tile_group_scan_kernel<<<(n_tiles + 255) / 256, 256, 0, s>>>(gsum, n_groups, n_tiles, total);
+        tile_group_scan_kernel<<<(n_cells + 255) / 256, 256, 0, s>>>(gsum, n_groups, n_cells, ctot);
         VEGS_CHECK_LAUNCH();
         tb = tb0;
-        VEGS_CUDA(cub::DeviceScan::ExclusiveSum(tmp, tb, total, tile_start, n_tiles, s));
-        chunk_offsets_kernel<<<(int)((ng + 255) / 256), 256, 0, s>>>(counts, gsum, tile_start, total, n_chunks,
-                                                                     n_tiles, G, tile_end);
+        VEGS_CUDA(cub::DeviceScan::ExclusiveSum(tmp, tb, ctot, c_start, n_cells, s));
+        chunk_offsets_kernel<<<(int)((ng + 255) / 256), 256, 0, s>>>(counts, gsum, c_start, ctot, n_chunks,
+                                                                     n_cells, G, c_end);
         VEGS_CHECK_LAUNCH();
-        // 3. placement, one warp per chunk
-        if (n_tiles <= 4096)
-            place_kernel<8><<<n_chunks, 32 * 8, sizeof(uint32_t) * n_tiles, s>>>(ids, bin_rect, n_kept, C,
-                                                                               tiles_x, tiles_y, counts, sorted_gauss,
-                                                                               n_kept_dev);
+        // 3. placement, one warp per chunk and band of cell rows
+        uint32_t *dst = two ? coarse : sorted_gauss;
+        if (n_cells <= 4096 && !two)
+            place_kernel<8><<<n_chunks, 32 * 8, sizeof(uint32_t) * n_cells, s>>>(ids, bin_rect, n_kept, C, cells_x,
+                                                                               cells_y, counts, dst, n_kept_dev,
+                                                                               cell_shift);
         else
-            place_kernel<4><<<n_chunks, 32 * 4, sizeof(uint32_t) * n_tiles, s>>>(ids, bin_rect, n_kept, C,
-                                                                               tiles_x, tiles_y, counts, sorted_gauss,
-                                                                               n_kept_dev);
+            place_kernel<4><<<n_chunks, 32 * 4, sizeof(uint32_t) * n_cells, s>>>(ids, bin_rect, n_kept, C, cells_x,
+                                                                               cells_y, counts, dst, n_kept_dev,
+                                                                               cell_shift);
         VEGS_CHECK_LAUNCH();
+        if (two) {  // 4. level 2: per block, its tiles' counts, the tile ranges, the runs
+            int *tdiff = (int *)gsum;  // the level-1 group sums are consumed: reuse for the tile difference array
+            VEGS_CUDA(cudaMemsetAsync(tdiff, 0, sizeof(int) * (size_t)(tiles_x + 1) * (tiles_y + 1), s));
+            int diff_blocks = (int)((n_kept + 1023) / 1024);
+            diff_blocks = diff_blocks < 148 * 2 ? diff_blocks : 148 * 2;
+            const size_t tdiff_bytes = sizeof(int) * (size_t)(tiles_x + 1) * (tiles_y + 1);
+            tile_diff_kernel<<<diff_blocks, 256, tdiff_bytes, s>>>(ids, bin_rect, n_kept, tiles_x, tiles_y, tdiff,
+                                                                  n_kept_dev);
+            VEGS_CHECK_LAUNCH();
+            tile_total_kernel<<<1, 1024, tdiff_bytes, s>>>(tdiff, tiles_x, tiles_y, total);
+            VEGS_CHECK_LAUNCH();
+            tb = tb0;
+            VEGS_CUDA(cub::DeviceScan::ExclusiveSum(tmp, tb, total, tile_start, n_tiles, s));
+            block_place_kernel<<<n_blk, 256, 0, s>>>(coarse, cstart, cend, bin_rect, tiles_x, tiles_y, bx, tile_start,
+                                                     tile_end, sorted_gauss);
+            VEGS_CHECK_LAUNCH();
+        }
         if ((inst_pid || order) && !counts_dev && !cull_record) {
             placed_extras_kernel<<<(int)((n_inst + 255) / 256), 256, 0, s>>>(
                 sorted_gauss, (const int4 *)rect, offsets, kept_idx, tile_end, n_inst, n_tiles, tiles_x, inst_pid,
@@ -768,11 +960,12 @@ extern "C" int vegs_bin_count_dev(uint32_t *tiles, int64_t n, int64_t *offsets, 
 
 extern "C" int vegs_bin_sort_dev(const uint64_t *depth_key, const int32_t *rect, const int64_t *offsets,
                                  const int64_t *kept_idx, int64_t n, const int64_t *counts, int64_t kept_capacity,
+                                 int64_t inst_capacity,
                                  int32_t width, int32_t height, int32_t tile_size, uint32_t *sorted_gauss,
                                  int32_t *tile_start, int32_t *tile_end, int32_t *tile_order,
                                  const float *cull_record, int32_t n_channels, void *ws, size_t *ws_bytes,
                                  void *stream) {
-    if (!ws_bytes || tile_size != kTile || width < 1 || height < 1 || !counts) return VEGS_ERR_ARG;
+    if (!ws_bytes || tile_size != kTile || width < 1 || height < 1 || !counts || inst_capacity < 0) return VEGS_ERR_ARG;
     if (cull_record && n_channels != 3 && n_channels != 11) return VEGS_ERR_ARG;
     if (n >= (int64_t(1) << 31)) return VEGS_ERR_ARG;
     const int tiles_x = (width + kTile - 1) / kTile, tiles_y = (height + kTile - 1) / kTile;
@@ -782,5 +975,5 @@ extern "C" int vegs_bin_sort_dev(const uint64_t *depth_key, const int32_t *rect,
     const int64_t kc = kept_capacity < n ? kept_capacity : n;
     return bin_place_impl(depth_key, rect, offsets, kept_idx, n, kc, 1, tiles_x, tiles_y, sorted_gauss, nullptr,
                           nullptr, tile_start, tile_end, tile_order, ws, ws_bytes, (cudaStream_t)stream, counts,
-                          cull_record, cull_record ? rec_stride(n_channels) : 0);
+                          cull_record, cull_record ? rec_stride(n_channels) : 0, inst_capacity);
 }

@@ -42,8 +42,9 @@ LAUNCHES = {
     "vegs_bin_sort_dev": 18,      # the placement path of vegs_bin_sort
     "vegs_bin_sort": 18,          # counting placement: coarse keys, CUB depth sort (hist + scan + 4 onesweep), ties,
                                   # chunk counts, group sums, group scan, CUB scan (2), chunk offsets, placement,
-                                  # tile weights + single-tile CUB sort (heaviest-first tile order); +1 (order /
-                                  # inst_pid) on the API path.  Radix path (> 12288 tiles): 19.
+                                  # tile weights + single-tile CUB sort (heaviest-first tile order); +5 from 4096
+                                  # tiles (two levels: tile difference array, its prefix sums, CUB scan (2), block
+                                  # runs); +1 (order / inst_pid) on the API path.  Radix path (> 12288 tiles): 19.
     "vegs_composite_forward": 1,
     "vegs_composite_forward_fast": 2,  # blend + float64 fix-up of the undecidable pixels (+ a 4-byte memset)
     "vegs_composite_backward": 1,
@@ -267,6 +268,13 @@ class Rasterizer:
         tx, ty = (width + TILE - 1) // TILE, (height + TILE - 1) // TILE
         return (tx + 1) * (ty + 1) <= 12288 and os.environ.get("VEGS_BIN_RADIX", "")[:1] in ("", "0")
 
+    @staticmethod
+    def _two_level(width: int, height: int) -> bool:
+        """Two-level placement (the C library's rule: from 4096 tiles, VEGS_PLACE_FLAT overrides)."""
+        env = os.environ.get("VEGS_PLACE_FLAT", "")[:1]
+        tiles = ((width + TILE - 1) // TILE) * ((height + TILE - 1) // TILE)
+        return env == "0" if env else tiles >= 4096
+
     def _culls(self) -> bool:
         """Culled binning (tight ellipse boxes, float32 tables): tile lists hold only the
         instances that can blend in their tile.  Same images and gradients; out_last and the
@@ -381,12 +389,13 @@ class Rasterizer:
             n_kept, n_inst = int(self.kept_cap), int(self.inst_cap)  # capacities (the counts stay on the device)
             sorted_gauss = A.get("sorted_gauss", n_inst, torch.int32)
             args = (_p(depth_key), _p(rect), _p(offsets), _p(kept_idx), n, _p(pend["counts"]), int(self.kept_cap),
-                    width, height, TILE, _p(sorted_gauss), _p(tile_start), _p(tile_end), _p(tile_order),
+                    int(self.inst_cap), width, height, TILE, _p(sorted_gauss), _p(tile_start), _p(tile_end), _p(tile_order),
                     _p(record) if self._culls() else None, self.n_ch)
             wsz = _lib.size_query("vegs_bin_sort_dev", *args, tail=(s,))
             ws = A.get("ws_sort", wsz, torch.uint8)
             self._run("vegs_bin_sort_dev", *args, _p(ws), ctypes.byref(ctypes.c_size_t(wsz)), s)
-            self.launches += 2 + self._culls()  # the capacity check of vegs_bin_count_dev (+ the binning rects)
+            # the capacity check of vegs_bin_count_dev (+ the binning rects, + the second placement level)
+            self.launches += 2 + self._culls() + 5 * self._two_level(width, height)
         else:
             pend["event"].synchronize()
             n_kept, n_inst = (int(x) for x in pend["host"].tolist())
@@ -405,7 +414,9 @@ class Rasterizer:
                 self.launches += 1  # the binning rects
             if not self._placement(width, height):
                 self.launches += 1  # radix path
-            elif want_order:
+            elif self._two_level(width, height):
+                self.launches += 5  # the second placement level
+            if self._placement(width, height) and want_order:
                 self.launches += 1  # order / inst_pid for the reference-shaped API
         self.last_counts = (n_kept, n_inst)
         hw = width * height

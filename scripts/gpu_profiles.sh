@@ -1,10 +1,10 @@
 #!/bin/bash
-# GPU box: v31 (culled binning) -- GPU tests, ncu full captures of the compositing kernels
+# GPU box (V=vNN): GPU tests, ncu full captures of the compositing kernels
 # (one c2 training view; one 3M / 1080p config-3 render) summarised here, the bench with the
 # fresh capture in profiles/, and the launch lists of one training step and of the bench command.
 mkdir -p gpurun_out
 NCU=/usr/local/cuda/bin/ncu
-V=v31
+V=${V:-v32}
 timeout 1500 python -m pytest tests -q -m gpu -p no:cacheprovider > gpurun_out/gpu_tests.log 2>&1
 echo "pytest rc=$?" >> gpurun_out/gpu_tests.log
 timeout 600 python scripts/profile_step.py --views 1 > gpurun_out/prof_plain1.log 2>&1 && \
@@ -33,7 +33,7 @@ echo "launch-list rc=$?" >> gpurun_out/ncu_launch.log
 python scripts/launch_summary.py /tmp/launches_$V.csv > gpurun_out/launches_${V}_summary.txt 2>&1
 gzip -c /tmp/launches_$V.csv > gpurun_out/launches_$V.csv.gz
 timeout 1800 $NCU --metrics gpu__time_duration.sum --clock-control none --csv \
-    --log-file /tmp/bench_cmd_launches_$V.csv python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-api \
+    --log-file /tmp/bench_cmd_launches_$V.csv python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-api --c4-steps 2 --sweep-frames 1 --render-frames 1 \
     > gpurun_out/ncu_bench.log 2>&1
 echo "bench-cmd rc=$?" >> gpurun_out/ncu_bench.log
 python scripts/launch_summary.py /tmp/bench_cmd_launches_$V.csv > gpurun_out/bench_cmd_launches_${V}_summary.txt 2>&1

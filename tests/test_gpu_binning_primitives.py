@@ -51,3 +51,26 @@ def test_tile_launch_order_is_heaviest_first_stable(wh):
     c = (fr.tile_end - fr.tile_start).cpu().numpy().astype(np.int64)
     key = 0xFFFF - np.minimum(c, 0xFFFF)
     assert np.array_equal(fr.tile_order.cpu().numpy(), np.argsort(key, kind="stable"))
+
+
+@pytest.mark.parametrize("wh", [(1024, 1024), (1000, 700), (200, 120), (1920, 1080)])
+@pytest.mark.parametrize("cull", [False, True])
+def test_two_level_placement_equals_single_level(monkeypatch, wh, cull):
+    """The two-level placement (4x4-tile blocks, then runs per tile) builds exactly the tile
+    lists of the single-level placement (VEGS_PLACE_FLAT=1): same ranges, same ids in the
+    same order, on grids that are and are not multiples of the block."""
+    from paper_2504_13339_b200 import scenes
+    from paper_2504_13339_b200.device import DeviceTF, Rasterizer
+
+    gs = scenes.blob_gaussians(150_000, seed=3)
+    cam = scenes.orbit_cameras(1, 5, *wh)[0]
+    params = torch.from_numpy(gs.pack()).cuda()
+    tf = DeviceTF(scenes.random_tf(9))
+    out = []
+    for flat in ("1", "0"):
+        monkeypatch.setenv("VEGS_PLACE_FLAT", flat)
+        fr = Rasterizer(pooled=False, cull=cull).forward(params, len(gs), tf, cam)
+        listed = int(fr.tile_end.max())
+        out.append((fr.tile_start.clone(), fr.tile_end.clone(), fr.sorted_gauss[:listed].clone(), fr.out_img.clone()))
+    for a, b in zip(out[0], out[1]):
+        assert torch.equal(a, b)
