@@ -10,7 +10,7 @@ for flat in 0 1; do
       --csv python scripts/profile_render.py --config $cfg > gpurun_out/p2_${cfg}_$flat.csv 2>&1
   done
 done
-for v in "VEGS_X=0" "VEGS_PLACE_FLAT=1" "VEGS_PLACE_FLAT=0" "VEGS_X=0" "VEGS_PLACE_FLAT=1" "VEGS_PLACE_FLAT=0"; do
+for v in "VEGS_X=0" "VEGS_PLACE_FLAT=1" "VEGS_X=0" "VEGS_PLACE_FLAT=1"; do
   echo "== $v" >> gpurun_out/p2_bench.log
   env $v timeout 900 python bench.py --steps 20 --warmup 5 --no-api --no-cpu-baseline 2>&1 | tail -1 > /tmp/b.json
   python - >> gpurun_out/p2_bench.log <<'PY'
