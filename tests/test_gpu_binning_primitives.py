@@ -63,6 +63,7 @@ def test_two_level_placement_equals_single_level(monkeypatch, wh, cull):
     from paper_2504_13339_b200.device import DeviceTF, Rasterizer
 
     gs = scenes.blob_gaussians(150_000, seed=3)
+    gs.log_scale[:300] += 2.5  # a few splats spanning many blocks (full 16-tile masks)
     cam = scenes.orbit_cameras(1, 5, *wh)[0]
     params = torch.from_numpy(gs.pack()).cuda()
     tf = DeviceTF(scenes.random_tf(9))

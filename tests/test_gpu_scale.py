@@ -584,6 +584,23 @@ def test_graph_steps_bitwise_equal_eager_steps():
     assert len(tr._graphs) == 1 and all(l.rz.inst_cap > 0 for l in tr.lanes)
 
 
+@pytest.mark.parametrize("flat", ["0", "1"])
+def test_graph_steps_both_placements(monkeypatch, flat):
+    """Graph-replayed device-count steps through the two-level placement (forced on small
+    views with VEGS_PLACE_FLAT=0; 4096+ tiles take it by default) and the single level give
+    bitwise the eager steps of the other placement: the placement changes no list."""
+    learned, dtf, cams, targets = _train_scene(4, 144, 112)
+    views = [View(c, dtf, t) for c, t in zip(cams, targets)]
+    monkeypatch.setenv("VEGS_PLACE_FLAT", flat)
+    tr = Trainer(learned, TrainConfig(iterations=100), graphs=True)
+    lg = [float(tr.step(views, iteration=s + 1).item()) for s in range(3)]
+    pg = tr.params.clone()
+    monkeypatch.setenv("VEGS_PLACE_FLAT", "1" if flat == "0" else "0")
+    te = Trainer(learned, TrainConfig(iterations=100), graphs=False)
+    le = [float(te.step(views, iteration=s + 1).item()) for s in range(3)]
+    assert lg == le and torch.equal(pg, te.params) and len(tr._graphs) == 1
+
+
 def test_graph_steps_with_alternating_views_and_host_targets():
     """Two alternating sets of views (two cached graphs), pinned host targets uploaded inside
     the graph, and DensifyStats tracking: bitwise the eager run."""
