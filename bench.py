@@ -70,6 +70,8 @@ def parse():
     ap.add_argument("--lanes", type=int, default=4, help="CUDA-stream lanes of the view pipeline")
     ap.add_argument("--no-cull", action="store_true",
                     help="bin on the reference's whole rects (default: tight ellipse boxes, identical results)")
+    ap.add_argument("--no-shared-projection", action="store_true",
+                    help="config-3 sweep: preprocess every (frame, TF) in full instead of projecting each frame once")
     ap.add_argument("--no-graphs", action="store_true",
                     help="host-counted eager steps instead of device-count steps replayed as CUDA graphs")
     ap.add_argument("--backend", choices=("nccl", "gloo"), default="nccl",
@@ -608,7 +610,7 @@ def run_sweep(args, dev, rank, world) -> dict:
     tfs = {f: [DeviceTF(scenes.random_tf(1000 + 8 * f + k), dev) for k in range(8)] for f in mine}
     from paper_2504_13339_b200.device import RenderPipeline
 
-    pipe = RenderPipeline(lanes=args.lanes, cull=not args.no_cull)
+    pipe = RenderPipeline(lanes=args.lanes, cull=not args.no_cull, project_once=not args.no_shared_projection)
     items = [(cams[f], tf) for f in mine for tf in tfs[f]]
     # warm-up over every (frame, TF): the scratch pools grow to the largest instance count
     # here, so no allocation happens inside the timed region

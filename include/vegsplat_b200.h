@@ -125,6 +125,17 @@ int vegs_preprocess_forward(const double *params, int64_t n, const VegsCamera *c
                             const VegsTF *tf, const VegsSettings *st, int32_t n_channels,
                             int32_t store_f64, VegsSplatTable *out, void *stream);
 
+/* The TF-independent half of the preprocess for one camera: proj (n x 8 float64: px, py,
+ * conic a b c, the footprint's major eigenvalue, view depth, front/positive-definite flag).
+ * vegs_preprocess_forward_projected = vegs_preprocess_forward taking that projection instead
+ * of recomputing it (a sweep of several TFs through one camera projects once); identical
+ * tables.  out->aux must be NULL there. */
+int vegs_project(const double *params, int64_t n, const VegsCamera *cam, const VegsSettings *st, double *proj,
+                 void *stream);
+int vegs_preprocess_forward_projected(const double *params, int64_t n, const VegsCamera *cam, const VegsTF *tf,
+                                      const VegsSettings *st, int32_t n_channels, int32_t store_f64,
+                                      const double *proj, VegsSplatTable *out, void *stream);
+
 /* Splat table from already-projected splats (the reference's SplatData, pipeline.py:40-49):
  * m rows of float64 mean2d (m x 2), conic (m x 3), alpha_base, depth, channels (m x C) and
  * int32 rect (m x 4).  Every row counts as kept.  Same record / key layout as above. */

@@ -78,6 +78,9 @@ _SIGS = {
     "vegs_adam_step": [P, P, P, P, c_int64, P, c_double, c_double, c_double, P, P],
     "vegs_adam_step_sum": [P, P, P, P, P, P, P, c_int64, P, c_double, P, P, P],
     "vegs_grad_pack": [P, P, P, P, P, c_int64, c_int32, c_int32, P],
+    "vegs_project": [P, c_int64, POINTER(VegsCamera), POINTER(VegsSettings), P, P],
+    "vegs_preprocess_forward_projected": [P, c_int64, POINTER(VegsCamera), POINTER(VegsTF), POINTER(VegsSettings),
+                                          c_int32, c_int32, P, POINTER(VegsSplatTable), P],
     "vegs_adam_step_range": [P, P, P, P, P, c_int64, c_int32, c_int32, P, P, P, P],
     "vegs_bin_count_dev": [P, c_int64, P, P, P, c_int64, c_int64, P, P, P, POINTER(c_size_t), P],
     "vegs_bin_sort_dev": [P, P, P, P, c_int64, P, c_int64, c_int64, c_int32, c_int32, c_int32, P, P, P, P, P,

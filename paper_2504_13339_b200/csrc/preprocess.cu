@@ -30,7 +30,7 @@ template <typename Real>
 #endif
 __global__ void __launch_bounds__(VEGS_PFWD_T, VEGS_PFWD_MINB) preprocess_fwd_kernel(
     const double *params, int64_t n, VegsCamera cam, VegsTF tf, VegsSettings st, int n_ch,
-    VegsSplatTable out) {
+    VegsSplatTable out, const double *proj) {
     extern __shared__ double tf_smem[];
     const TFTable tab = stage_tf(tf, tf_smem);
     const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -45,7 +45,20 @@ __global__ void __launch_bounds__(VEGS_PFWD_T, VEGS_PFWD_MINB) preprocess_fwd_ke
     bool kept = false;
     Projected p;
     if (s.visible) {
-        project_one(P, g, s.alpha_base, cam, st, p);
+        if (proj) {  // the camera's projection from vegs_project (TF-independent), then the rect
+            const double *c = proj + (int64_t)kProjStride * g;
+            p.px = c[0];
+            p.py = c[1];
+            p.conic[0] = c[2];
+            p.conic[1] = c[3];
+            p.conic[2] = c[4];
+            p.lam = c[5];
+            p.t[2] = c[6];
+            p.radius = st.radius_sigma * sqrt(fmax(p.lam, 0.0));
+            project_rect(s.alpha_base, cam, st, c[7] != 0.0, p);
+        } else {
+            project_one(P, g, s.alpha_base, cam, st, p);
+        }
         kept = p.keep;
     }
     if (out.aux) {
@@ -106,6 +119,29 @@ __global__ void __launch_bounds__(256) table_from_arrays_kernel(
     Real *r = reinterpret_cast<Real *>(out.record) + (int64_t)rec_stride(n_ch) * i;
     write_record(r, mean2d[2 * i], mean2d[2 * i + 1], conic + 3 * i, alpha_base[i], st.alpha_skip);
     for (int c = 0; c < n_ch; ++c) r[7 + c] = (Real)channels[(int64_t)n_ch * i + c];
+}
+
+// The TF-independent part of the preprocess for one camera (projection.py:43-176 up to the
+// conic): px, py, conic, the footprint's major eigenvalue, view depth and the front / positive-
+// definite flag, float64, kProjStride per Gaussian.  A sweep of several TFs through one camera
+// projects once and each TF's preprocess only shades and takes the level-set rect
+// (project_rect); the arithmetic is project_one's, so the tables are identical.
+__global__ void __launch_bounds__(256) project_kernel(const double *params, int64_t n, VegsCamera cam,
+                                                      VegsSettings st, double *proj) {
+    const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (g >= n) return;
+    const ParamView P(params, n);
+    Projected p;
+    project_one<false>(P, g, 0.0, cam, st, p);
+    double *c = proj + (int64_t)kProjStride * g;
+    c[0] = p.px;
+    c[1] = p.py;
+    c[2] = p.conic[0];
+    c[3] = p.conic[1];
+    c[4] = p.conic[2];
+    c[5] = p.lam;
+    c[6] = p.t[2];
+    c[7] = p.keep ? 1.0 : 0.0;
 }
 
 __global__ void tf_eval_kernel(const double *ts, const double *vals, int k, int n_cols,
@@ -204,9 +240,36 @@ extern "C" int vegs_tf_eval(const double *ts, const double *vals, int32_t n_knot
     return VEGS_OK;
 }
 
+static int preprocess_launch(const double *params, int64_t n, const VegsCamera *cam, const VegsTF *tf,
+                             const VegsSettings *st, int32_t n_channels, int32_t store_f64, VegsSplatTable *out,
+                             const double *proj, void *stream);
+
 extern "C" int vegs_preprocess_forward(const double *params, int64_t n, const VegsCamera *cam,
                                        const VegsTF *tf, const VegsSettings *st, int32_t n_channels,
                                        int32_t store_f64, VegsSplatTable *out, void *stream) {
+    return preprocess_launch(params, n, cam, tf, st, n_channels, store_f64, out, nullptr, stream);
+}
+
+extern "C" int vegs_project(const double *params, int64_t n, const VegsCamera *cam, const VegsSettings *st,
+                            double *proj, void *stream) {
+    if (!cam || !st || (n > 0 && (!params || !proj))) return VEGS_ERR_ARG;
+    if (n == 0) return VEGS_OK;
+    project_kernel<<<(int)((n + 255) / 256), 256, 0, (cudaStream_t)stream>>>(params, n, *cam, *st, proj);
+    VEGS_CHECK_LAUNCH();
+    return VEGS_OK;
+}
+
+extern "C" int vegs_preprocess_forward_projected(const double *params, int64_t n, const VegsCamera *cam,
+                                                 const VegsTF *tf, const VegsSettings *st, int32_t n_channels,
+                                                 int32_t store_f64, const double *proj, VegsSplatTable *out,
+                                                 void *stream) {
+    if ((n > 0 && !proj) || (out && out->aux)) return VEGS_ERR_ARG;  // aux views need the full projection
+    return preprocess_launch(params, n, cam, tf, st, n_channels, store_f64, out, proj, stream);
+}
+
+static int preprocess_launch(const double *params, int64_t n, const VegsCamera *cam, const VegsTF *tf,
+                             const VegsSettings *st, int32_t n_channels, int32_t store_f64, VegsSplatTable *out,
+                             const double *proj, void *stream) {
     if (!cam || !st || !out || !tf_ok(tf) || (n > 0 && !params)) return VEGS_ERR_ARG;
     if (n_channels != 3 && n_channels != 11) return VEGS_ERR_ARG;
     if (st->tile_size != kTile) return VEGS_ERR_ARG;
@@ -217,11 +280,11 @@ extern "C" int vegs_preprocess_forward(const double *params, int64_t n, const Ve
     if (store_f64) {
         VEGS_CUDA(cudaFuncSetAttribute(preprocess_fwd_kernel<double>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        preprocess_fwd_kernel<double><<<(int)((n + VEGS_PFWD_T - 1) / VEGS_PFWD_T), VEGS_PFWD_T, smem, s>>>(params, n, *cam, *tf, *st, n_channels, *out);
+        preprocess_fwd_kernel<double><<<(int)((n + VEGS_PFWD_T - 1) / VEGS_PFWD_T), VEGS_PFWD_T, smem, s>>>(params, n, *cam, *tf, *st, n_channels, *out, proj);
     } else {
         VEGS_CUDA(cudaFuncSetAttribute(preprocess_fwd_kernel<float>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        preprocess_fwd_kernel<float><<<(int)((n + VEGS_PFWD_T - 1) / VEGS_PFWD_T), VEGS_PFWD_T, smem, s>>>(params, n, *cam, *tf, *st, n_channels, *out);
+        preprocess_fwd_kernel<float><<<(int)((n + VEGS_PFWD_T - 1) / VEGS_PFWD_T), VEGS_PFWD_T, smem, s>>>(params, n, *cam, *tf, *st, n_channels, *out, proj);
     }
     VEGS_CHECK_LAUNCH();
     return VEGS_OK;

@@ -199,6 +199,9 @@ __device__ void shade_one(const PV &P, int64_t g, const TFTable &tf, const VegsC
     s.visible = s.alpha_base >= st.cull_alpha;
 }
 
+__device__ __forceinline__ void project_rect(double alpha_base, const VegsCamera &cam, const VegsSettings &st,
+                                             bool front_ok, Projected &p);
+
 template <bool kRect = true, class PV>
 __device__ void project_one(const PV &P, int64_t g, double alpha_base, const VegsCamera &cam,
                             const VegsSettings &st, Projected &p) {
@@ -279,6 +282,14 @@ __device__ void project_one(const PV &P, int64_t g, double alpha_base, const Veg
         p.keep = front && (p.det > 0);
         return;
     }
+    project_rect(alpha_base, cam, st, front && (p.det > 0), p);
+}
+
+// The level-set rectangle of a projected splat and its keep flag (the TF-dependent tail of
+// project_one: the radius follows the activated opacity).  front_ok = in front of the near
+// plane with a positive-definite footprint.
+__device__ __forceinline__ void project_rect(double alpha_base, const VegsCamera &cam, const VegsSettings &st,
+                                             bool front_ok, Projected &p) {
     const double ratio = fmax(alpha_base, st.alpha_skip) / st.alpha_skip;
     const double rc = sqrt(fmax(p.lam, 0.0) * 2.0 * log(ratio)) + st.rect_margin_px;
     const double Wd = (double)cam.width, Hd = (double)cam.height;
@@ -291,7 +302,7 @@ __device__ void project_one(const PV &P, int64_t g, double alpha_base, const Veg
     p.x1 = finite ? (int)fx1 : 0;
     p.y0 = finite ? (int)fy0 : 0;
     p.y1 = finite ? (int)fy1 : 0;
-    p.keep = front && (p.det > 0) && (p.x1 > p.x0) && (p.y1 > p.y0) && finite;
+    p.keep = front_ok && (p.x1 > p.x0) && (p.y1 > p.y0) && finite;
 }
 
 // Total order on float64 -> uint64 (negative values flipped), so a radix sort of the

@@ -25,6 +25,7 @@ constexpr double kBetaMin = 1.0, kBetaMax = 128.0;
 
 __host__ __device__ inline int rec_stride(int n_ch) { return ((7 + n_ch) + 3) & ~3; }
 __host__ __device__ inline int row_width(int n_ch) { return 6 + n_ch; }
+constexpr int kProjStride = 8;  // float64 per Gaussian in a vegs_project table
 
 // Class-major parameter layout (model.py FIELD_LAYOUT): element offsets for n Gaussians.
 struct ParamView {

@@ -36,6 +36,8 @@ TILE = 16
 # libvegsplat_b200.so); checked against the ncu launch list in profiles/.
 LAUNCHES = {
     "vegs_preprocess_forward": 1,
+    "vegs_preprocess_forward_projected": 1,
+    "vegs_project": 1,
     "vegs_splat_table_from_arrays": 1,
     "vegs_bin_count": 4,          # pack, CUB scan (init + sweep), unpack
     "vegs_bin_count_dev": 4,      # the same (+2 capacity-check launches counted in forward_end)
@@ -294,7 +296,7 @@ class Rasterizer:
 
     # -- forward --------------------------------------------------------------------
     def forward_begin(self, params: torch.Tensor, n: int, tf: DeviceTF, cam, background=(1.0, 1.0, 1.0),
-                      want_order: bool = False, api_views: bool = False) -> dict:
+                      want_order: bool = False, api_views: bool = False, proj: torch.Tensor | None = None) -> dict:
         """First half of a forward: preprocess + instance count, with the count copied to
         pinned host memory asynchronously.  ``forward_end`` waits for it and finishes; a
         caller can queue other streams' work in between (see Trainer)."""
@@ -314,8 +316,14 @@ class Rasterizer:
             for k, v in api.items():
                 setattr(tab, k, _p(v))
         cs = camera_struct(cam)
-        self._run("vegs_preprocess_forward", _p(params), n, ctypes.byref(cs), ctypes.byref(tf.struct),
-             ctypes.byref(self.st), self.n_ch, int(self.store_f64), ctypes.byref(tab), _stream())
+        if proj is not None:  # this camera's projection, computed once for several TFs (RenderPipeline)
+            if api_views:
+                raise ValueError("api_views needs the full preprocess (no shared projection)")
+            self._run("vegs_preprocess_forward_projected", _p(params), n, ctypes.byref(cs), ctypes.byref(tf.struct),
+                      ctypes.byref(self.st), self.n_ch, int(self.store_f64), _p(proj), ctypes.byref(tab), _stream())
+        else:
+            self._run("vegs_preprocess_forward", _p(params), n, ctypes.byref(cs), ctypes.byref(tf.struct),
+                      ctypes.byref(self.st), self.n_ch, int(self.store_f64), ctypes.byref(tab), _stream())
         return self._bin_begin(A, n, record, rect, tiles, depth_key, cam.width, cam.height, background, cs, tf,
                                params, want_order, api)
 
@@ -585,7 +593,7 @@ class RenderPipeline:
     Output frames are only valid until the lane that produced them is reused."""
 
     def __init__(self, settings: RasterSettings = DEFAULT_SETTINGS, n_channels: int = 3, lanes: int = 4,
-                 fast_t: bool = False, cull: bool = True):
+                 fast_t: bool = False, cull: bool = True, project_once: bool = True):
         dev = self.device = require_cuda()
         main = torch.cuda.current_stream(dev)
         self.lanes = [(main if i == 0 else torch.cuda.Stream(dev),
@@ -593,11 +601,29 @@ class RenderPipeline:
                       for i in range(max(1, lanes))]
         for _, rz in self.lanes:
             rz.contrib_counts = False  # images only
+        # project_once: items sharing a camera object (a TF sweep) share one projection
+        # (vegs_project), each TF then only shades and takes its rect; identical frames
+        self.project_once = project_once
+        self._proj_pool = Pool(dev)
+        self.launches = 0
 
     def render(self, params: torch.Tensor, n: int, items, background=(1.0, 1.0, 1.0), on_frame=None) -> int:
         """items: list of (camera, DeviceTF).  on_frame(i, frame) is called (on the frame's
         stream) right after each composite.  Returns the total instance count."""
         main = torch.cuda.current_stream(self.device)
+        proj = {}
+        if self.project_once:  # cameras used by several items: projected once, on the caller's stream
+            uses: dict = {}
+            for cam, _ in items:
+                uses[id(cam)] = uses.get(id(cam), 0) + 1
+            st = self.lanes[0][1].st
+            for cam, _ in items:
+                if uses[id(cam)] > 1 and id(cam) not in proj:
+                    buf = self._proj_pool.get(f"proj{len(proj)}", 8 * n, torch.float64)
+                    call("vegs_project", _p(params), n, ctypes.byref(camera_struct(cam)), ctypes.byref(st), _p(buf),
+                         _stream())
+                    self.launches += 1
+                    proj[id(cam)] = buf
         for i, (s, _) in enumerate(self.lanes):
             if i or s != main:  # lane 0 is the construction-time stream
                 s.wait_stream(main)
@@ -607,7 +633,8 @@ class RenderPipeline:
         def begin(i):
             s, rz = self.lanes[i % L]
             with use_stream(s):
-                pend[i] = rz.forward_begin(params, n, items[i][1], items[i][0], background)
+                pend[i] = rz.forward_begin(params, n, items[i][1], items[i][0], background,
+                                           proj=proj.get(id(items[i][0])))
 
         total = 0
         ahead = L > 1  # one lane: item i+1 must not overwrite item i's pooled table early

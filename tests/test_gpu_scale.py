@@ -194,6 +194,32 @@ def test_render_pipeline_frames_equal_single_stream(lanes):
             assert torch.equal(gi, img) and torch.equal(gt, t) and torch.equal(gl, last), (lanes, i)
 
 
+def test_render_pipeline_shared_projection_identical_frames():
+    """A TF sweep through RenderPipeline projects each camera once (vegs_project) and only
+    shades per TF (vegs_preprocess_forward_projected): frames bitwise those of full
+    preprocesses, item by item."""
+    gs = scenes.blob_gaussians(120_000, seed=5)
+    params = torch.from_numpy(gs.pack()).cuda()
+    cams = scenes.orbit_cameras(2, 5, 400, 260)
+    tfs = [DeviceTF(scenes.random_tf(2000 + k)) for k in range(3)]
+    items = [(c, tf) for c in cams for tf in tfs]
+    got = {}
+    for shared in (False, True):
+        frames = {}
+
+        def keep(i, fr):
+            frames[i] = (fr.out_img.clone(), fr.out_t.clone(), fr.out_last.clone(), fr.tile_end.clone())
+
+        pipe = RenderPipeline(lanes=3, project_once=shared)
+        pipe.render(params, len(gs), items, on_frame=keep)
+        torch.cuda.synchronize()
+        got[shared] = frames
+        assert pipe.launches == (len(cams) if shared else 0)
+    for i in range(len(items)):
+        for a, b in zip(got[False][i], got[True][i]):
+            assert torch.equal(a, b), i
+
+
 def _last_gauss(fr):
     last = fr.out_last.long()
     return torch.where(last >= 0, fr.sorted_gauss[last.clamp(min=0)].long(), torch.full_like(last, -1))
