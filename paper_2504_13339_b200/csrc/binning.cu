@@ -416,6 +416,9 @@ __global__ void __launch_bounds__(32 * kBands) place_kernel(const uint32_t *ids,
 // write requests: 0.44 ms of a 1080p frame).  Result identical to the single level:
 // per tile, the splats in depth order.
 constexpr int kBlk = 4;  // tiles per block side
+#ifndef VEGS_L1_BANDS
+#define VEGS_L1_BANDS 1  // level 1: one warp per chunk (2: 908, 4: 887 Mpx/s config-3 sweep against 913)
+#endif
 
 __device__ __forceinline__ uint32_t block_tile_mask(int4 q, int bx0, int by0, int tiles_x, int tiles_y) {
     if (q.y <= q.x || q.w <= q.z) return 0u;
@@ -474,11 +477,17 @@ __global__ void __launch_bounds__(1024) tile_total_kernel(const int *diff, int t
 
 // level 2: the block's tiles filled run by run (the next batch's ids and rects are fetched
 // while one is placed); tile_end from the final cursors
-__global__ void __launch_bounds__(256) block_place_kernel(const uint32_t *coarse, const int32_t *blk_start,
+#ifndef VEGS_BP_T
+#define VEGS_BP_T 512  // 16 warps per block CTA, one 512-splat sub-batch per batch (256 x 2: -2.6% sweep; 1024: -1%)
+#endif
+#ifndef VEGS_BP_K
+#define VEGS_BP_K 1
+#endif
+__global__ void __launch_bounds__(VEGS_BP_T) block_place_kernel(const uint32_t *coarse, const int32_t *blk_start,
                                                           const int32_t *blk_end, const int4 *rect, int tiles_x,
                                                           int tiles_y, int bx, const int32_t *tile_start,
                                                           int32_t *tile_end, uint32_t *sorted_gauss) {
-    constexpr int NB = kBlk * kBlk, NW = 8, K = 2;  // K splats per thread per batch
+    constexpr int NB = kBlk * kBlk, NT = VEGS_BP_T, NW = NT / 32, K = VEGS_BP_K;  // K splats per thread per batch
     __shared__ uint32_t s_cur[NB];      // next slot of each tile
     __shared__ uint32_t s_wc[NW][NB];   // per-warp counts of the batch, then the warps' first slots
     const int blk = blockIdx.x, bx0 = (blk % bx) * kBlk, by0 = (blk / bx) * kBlk;
@@ -489,28 +498,28 @@ __global__ void __launch_bounds__(256) block_place_kernel(const uint32_t *coarse
         s_cur[t] = tx < tiles_x && ty < tiles_y ? (uint32_t)tile_start[ty * tiles_x + tx] : 0u;
     }
     const int beg = blk_start[blk], end = blk_end[blk];
-    // batch layout: splat beg + i0 + k * 256 + t for k < K (each warp's splats stay in list order
+    // batch layout: splat beg + i0 + k * NT + t for k < K (each warp's splats stay in list order
     // per k; the K sub-batches are ranked one after the other)
     uint32_t g_n[K];
     int4 q_n[K];
     auto fetch = [&](int i0) {
 #pragma unroll
         for (int k = 0; k < K; ++k) {
-            const int i = i0 + k * 256 + t;
+            const int i = i0 + k * NT + t;
             g_n[k] = i < end ? coarse[i] : 0u;
             q_n[k] = i < end ? __ldg(rect + g_n[k]) : make_int4(0, 0, 0, 0);
         }
     };
     fetch(beg);
     __syncthreads();
-    for (int i0 = beg; i0 < end; i0 += K * 256) {  // block-uniform trip count
+    for (int i0 = beg; i0 < end; i0 += K * NT) {  // block-uniform trip count
         uint32_t g[K], m[K];
 #pragma unroll
         for (int k = 0; k < K; ++k) {
             g[k] = g_n[k];
             m[k] = block_tile_mask(q_n[k], bx0, by0, tiles_x, tiles_y);
         }
-        if (i0 + K * 256 < end) fetch(i0 + K * 256);
+        if (i0 + K * NT < end) fetch(i0 + K * NT);
 #pragma unroll
         for (int k = 0; k < K; ++k) {
             uint32_t bal[NB];
@@ -875,10 +884,13 @@ static int bin_place_impl(const uint64_t *depth_key, const int32_t *rect, const 
             place_kernel<8><<<n_chunks, 32 * 8, sizeof(uint32_t) * n_cells, s>>>(ids, bin_rect, n_kept, C, cells_x,
                                                                                cells_y, counts, dst, n_kept_dev,
                                                                                cell_shift);
-        else
+        else if (!two)
             place_kernel<4><<<n_chunks, 32 * 4, sizeof(uint32_t) * n_cells, s>>>(ids, bin_rect, n_kept, C, cells_x,
                                                                                cells_y, counts, dst, n_kept_dev,
                                                                                cell_shift);
+        else  // level 1 (a few block rows per band)
+            place_kernel<VEGS_L1_BANDS><<<n_chunks, 32 * VEGS_L1_BANDS, sizeof(uint32_t) * n_cells, s>>>(
+                ids, bin_rect, n_kept, C, cells_x, cells_y, counts, dst, n_kept_dev, cell_shift);
         VEGS_CHECK_LAUNCH();
         if (two) {  // 4. level 2: per block, its tiles' counts, the tile ranges, the runs
             int *tdiff = (int *)gsum;  // the level-1 group sums are consumed: reuse for the tile difference array
@@ -893,7 +905,7 @@ static int bin_place_impl(const uint64_t *depth_key, const int32_t *rect, const 
             VEGS_CHECK_LAUNCH();
             tb = tb0;
             VEGS_CUDA(cub::DeviceScan::ExclusiveSum(tmp, tb, total, tile_start, n_tiles, s));
-            block_place_kernel<<<n_blk, 256, 0, s>>>(coarse, cstart, cend, bin_rect, tiles_x, tiles_y, bx, tile_start,
+            block_place_kernel<<<n_blk, VEGS_BP_T, 0, s>>>(coarse, cstart, cend, bin_rect, tiles_x, tiles_y, bx, tile_start,
                                                      tile_end, sorted_gauss);
             VEGS_CHECK_LAUNCH();
         }
