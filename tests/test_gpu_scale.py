@@ -662,11 +662,12 @@ def test_graph_step_overflow_regrows_and_redoes():
     assert torch.equal(res[False][1], res[True][1])
 
 
-@pytest.mark.parametrize("lanes,aux", [(1, False), (2, True)])
+@pytest.mark.parametrize("lanes,aux", [(1, False), (2, True), (8, False)])
 def test_graph_steps_other_lane_counts_and_aux(lanes, aux):
-    """Graph-replayed steps with one lane (no look-ahead) and with the 11-plane aux loss:
-    bitwise the eager steps."""
-    learned, dtf, cams, targets = _train_scene(3)
+    """Graph-replayed steps with one lane (no look-ahead), with the 11-plane aux loss, and
+    with 8 lanes (config 4's; lane sums beyond four in a sum-only pass): bitwise the eager
+    steps."""
+    learned, dtf, cams, targets = _train_scene(10 if lanes == 8 else 3)
     views = [View(c, dtf, t) for c, t in zip(cams, targets)]
     res = _graph_runs(lambda s: views, 3, lanes=lanes, with_aux=aux)
     assert res[False][0] == res[True][0]
