@@ -240,6 +240,106 @@ __global__ void bin_rect_kernel(const float *record, int rs, const int4 *rect, i
     brect[i] = r;
 }
 
+// ---- small depth sorts in one CTA ----------------------------------------------------
+// Stable LSD radix sort of up to kSmallSort (key, id) pairs by 32-bit key in a single CTA
+// (4 passes of 8 bits, keys and ids in SMEM between passes): config-4 views keep ~11k
+// splats, where the device-wide sort's 6 launches are pure latency.  Ranking per warp with
+// match.any peer groups (items in index order: warp-major, item, lane), digit offsets by an
+// exclusive sum over the 256 digits; stable, so the same order as the device-wide sort.
+constexpr int kSmallSortT = 1024, kSmallSortItems = 16, kSmallSort = kSmallSortT * kSmallSortItems;
+
+__global__ void __launch_bounds__(kSmallSortT) small_sort_kernel(const uint32_t *keys, const uint32_t *vals, int n,
+                                                                 uint32_t *keys_out, uint32_t *vals_out) {
+    constexpr int NW = kSmallSortT / 32, IT = kSmallSortItems;
+    __shared__ uint32_t s_wc[NW][256];
+    __shared__ uint32_t s_dstart[256];
+    extern __shared__ uint32_t s_kv[];  // keys [0, n), ids [kSmallSort, kSmallSort + n)
+    const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+    const int items = (n + kSmallSortT - 1) / kSmallSortT;  // per thread (<= IT)
+    uint32_t key[IT], val[IT];
+#pragma unroll
+    for (int i = 0; i < IT; ++i) {
+        const int idx = w * 32 * items + i * 32 + lane;
+        const bool ok = i < items && idx < n;
+        key[i] = ok ? keys[idx] : 0u;
+        val[i] = ok ? vals[idx] : 0u;
+    }
+    for (int pass = 0; pass < 4; ++pass) {
+        const int shift = 8 * pass;
+        for (int i = t; i < NW * 256; i += kSmallSortT) (&s_wc[0][0])[i] = 0;
+        __syncthreads();
+        int dig[IT];
+        uint32_t rank[IT];
+#pragma unroll
+        for (int i = 0; i < IT; ++i) {
+            const int idx = w * 32 * items + i * 32 + lane;
+            dig[i] = i < items && idx < n ? (int)((key[i] >> shift) & 255u) : 256;
+            if (i >= items) continue;
+            const unsigned peers = __match_any_sync(0xffffffffu, dig[i]);
+            const uint32_t before = dig[i] < 256 ? s_wc[w][dig[i]] : 0u;
+            rank[i] = before + (uint32_t)__popc(peers & ((1u << lane) - 1u));
+            __syncwarp();
+            if (dig[i] < 256 && lane == __ffs(peers) - 1) s_wc[w][dig[i]] = before + (uint32_t)__popc(peers);
+            __syncwarp();
+        }
+        __syncthreads();
+        if (t < 256) {  // digit t: the warps' offsets and the digit's total
+            uint32_t cnt = 0;
+            for (int k = 0; k < NW; ++k) {
+                const uint32_t c = s_wc[k][t];
+                s_wc[k][t] = cnt;
+                cnt += c;
+            }
+            s_dstart[t] = cnt;
+        }
+        __syncthreads();
+        if (t < 32) {  // exclusive sum of the 256 digit totals (8 per lane)
+            uint32_t v[8], sum = 0;
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                v[q] = s_dstart[lane * 8 + q];
+                sum += v[q];
+            }
+            uint32_t x = sum;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+                if (lane >= o) x += y;
+            }
+            uint32_t run = x - sum;
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                s_dstart[lane * 8 + q] = run;
+                run += v[q];
+            }
+        }
+        __syncthreads();
+        const bool last = pass == 3;
+#pragma unroll
+        for (int i = 0; i < IT; ++i)
+            if (i < items && dig[i] < 256) {
+                const uint32_t pos = s_dstart[dig[i]] + s_wc[w][dig[i]] + rank[i];
+                if (last) {
+                    keys_out[pos] = key[i];
+                    vals_out[pos] = val[i];
+                } else {
+                    s_kv[pos] = key[i];
+                    s_kv[kSmallSort + pos] = val[i];
+                }
+            }
+        if (last) break;
+        __syncthreads();
+#pragma unroll
+        for (int i = 0; i < IT; ++i) {
+            const int idx = w * 32 * items + i * 32 + lane;
+            if (i < items && idx < n) {
+                key[i] = s_kv[idx];
+                val[i] = s_kv[kSmallSort + idx];
+            }
+        }
+    }
+}
+
 // ---- counting placement (no instance-level sort) ----------------------------------
 // The kept splats in depth order are cut into chunks of C.  (1) per chunk, per-tile
 // instance counts from a 2D difference array of the splats' tile rectangles; (2) those
@@ -849,7 +949,17 @@ static int bin_place_impl(const uint64_t *depth_key, const int32_t *rect, const 
         VEGS_CHECK_LAUNCH();
         cub::DoubleBuffer<uint32_t> dk(dk0, dk1), dv(id0, id1);
         size_t tb = tb0;
-        VEGS_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tb, dk, dv, n_sort, 0, 32, s));
+        const char *ss_env = getenv("VEGS_SMALL_SORT");  // "0": always the device-wide sort (tests)
+        if (n_sort <= kSmallSort && !(ss_env && ss_env[0] == '0')) {  // one CTA (config-4 sized views)
+            const int smem = (int)(2 * sizeof(uint32_t) * kSmallSort);
+            VEGS_CUDA(cudaFuncSetAttribute(small_sort_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+            small_sort_kernel<<<1, kSmallSortT, smem, s>>>(dk0, id0, (int)n_sort, dk1, id1);
+            VEGS_CHECK_LAUNCH();
+            dk.selector = 1;
+            dv.selector = 1;
+        } else {
+            VEGS_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tb, dk, dv, n_sort, 0, 32, s));
+        }
         depth_ties_kernel<<<(int)((n_kept + 255) / 256), 256, 0, s>>>(dk.Current(), depth_key, n_kept, dv.Current(),
                                                                      n_kept_dev);
         VEGS_CHECK_LAUNCH();

@@ -277,6 +277,11 @@ class Rasterizer:
         tiles = ((width + TILE - 1) // TILE) * ((height + TILE - 1) // TILE)
         return env == "0" if env else tiles >= 4096
 
+    @staticmethod
+    def _small_sort(n_sort: int) -> bool:
+        """The one-CTA depth sort (the C library's rule: <= 16384 keys, VEGS_SMALL_SORT=0 disables)."""
+        return n_sort <= 16384 and os.environ.get("VEGS_SMALL_SORT", "")[:1] != "0"
+
     def _culls(self) -> bool:
         """Culled binning (tight ellipse boxes, float32 tables): tile lists hold only the
         instances that can blend in their tile.  Same images and gradients; out_last and the
@@ -402,8 +407,10 @@ class Rasterizer:
             wsz = _lib.size_query("vegs_bin_sort_dev", *args, tail=(s,))
             ws = A.get("ws_sort", wsz, torch.uint8)
             self._run("vegs_bin_sort_dev", *args, _p(ws), ctypes.byref(ctypes.c_size_t(wsz)), s)
-            # the capacity check of vegs_bin_count_dev (+ the binning rects, + the second placement level)
-            self.launches += 2 + self._culls() + 5 * self._two_level(width, height)
+            # the capacity check of vegs_bin_count_dev (+ the binning rects, + the second placement
+            # level, - the device-wide depth sort's 6 launches for one when <= 16384 splats are sorted)
+            self.launches += 2 + self._culls() + 5 * self._two_level(width, height) - 5 * self._small_sort(
+                min(int(self.kept_cap), n))
         else:
             pend["event"].synchronize()
             n_kept, n_inst = (int(x) for x in pend["host"].tolist())
@@ -422,8 +429,8 @@ class Rasterizer:
                 self.launches += 1  # the binning rects
             if not self._placement(width, height):
                 self.launches += 1  # radix path
-            elif self._two_level(width, height):
-                self.launches += 5  # the second placement level
+            else:
+                self.launches += 5 * self._two_level(width, height) - 5 * self._small_sort(n)
             if self._placement(width, height) and want_order:
                 self.launches += 1  # order / inst_pid for the reference-shaped API
         self.last_counts = (n_kept, n_inst)

@@ -75,3 +75,24 @@ def test_two_level_placement_equals_single_level(monkeypatch, wh, cull):
         out.append((fr.tile_start.clone(), fr.tile_end.clone(), fr.sorted_gauss[:listed].clone(), fr.out_img.clone()))
     for a, b in zip(out[0], out[1]):
         assert torch.equal(a, b)
+
+
+@pytest.mark.parametrize("n", [5, 2000, 16_384])
+def test_small_depth_sort_equals_device_wide_sort(monkeypatch, n):
+    """Views with up to 16384 splats to sort take the one-CTA radix sort; its order (and so
+    every tile list) equals the device-wide sort's (VEGS_SMALL_SORT=0), ties included."""
+    from paper_2504_13339_b200 import scenes
+    from paper_2504_13339_b200.device import DeviceTF, Rasterizer
+
+    gs = scenes.random_gaussians(n, seed=11)
+    gs.position[: n // 4] = gs.position[0]  # equal depths: the stable order decides
+    cam = scenes.orbit_cameras(1, 3, 160, 120)[0]
+    params = torch.from_numpy(gs.pack()).cuda()
+    tf = DeviceTF(scenes.random_tf(2, 4))
+    out = []
+    for env in ("0", "1"):
+        monkeypatch.setenv("VEGS_SMALL_SORT", env)
+        fr = Rasterizer(pooled=False).forward(params, len(gs), tf, cam, want_order=True)
+        out.append((fr.tile_start.clone(), fr.tile_end.clone(), fr.order.clone(), fr.out_img.clone()))
+    for a, b in zip(out[0], out[1]):
+        assert torch.equal(a, b)
