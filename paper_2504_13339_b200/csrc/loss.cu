@@ -45,7 +45,10 @@ __device__ __forceinline__ float block_sum_f(float v, float *red) {
     return s;
 }
 
-__global__ void __launch_bounds__(VEGS_SSIM_T) ssim_fwd_kernel(const float *__restrict__ x, const float *__restrict__ y,
+#ifndef VEGS_SSIM_FWD_MINB
+#define VEGS_SSIM_FWD_MINB 3  // 80 registers (a 48-byte spill), 3 CTAs per SM: loss 0.133 -> 0.100 ms per c2 view (4: 0.101)
+#endif
+__global__ void __launch_bounds__(VEGS_SSIM_T, VEGS_SSIM_FWD_MINB) ssim_fwd_kernel(const float *__restrict__ x, const float *__restrict__ y,
                                                        int H, int W, int xs, Taps taps, float c1, float c2,
                                                        float coeff, float *__restrict__ maps, double *sums) {
     // (x, y) pairs interleaved so the two blurs of x and y (and of x^2, y^2) run as packed
