@@ -40,6 +40,10 @@
  *                             placement (the path views above 12288 tiles always take)
  *   VEGS_FAST_T_DEFER_ALL=1   vegs_composite_forward_fast hands every terminating pixel to its
  *                             float64 fix-up pass (exercises the fix-up)
+ *   VEGS_PLACE_FLAT=1 / =0    counting placement in one level / in two levels (4x4-tile blocks,
+ *                             then per-tile runs) regardless of the tile count (default: two
+ *                             levels from 4096 tiles); the tile lists are identical
+ *   VEGS_SMALL_SORT=0         the device-wide depth sort even for <= 16384 keys (default: one CTA)
  */
 #ifndef VEGSPLAT_B200_H
 #define VEGSPLAT_B200_H
