@@ -96,3 +96,37 @@ def test_small_depth_sort_equals_device_wide_sort(monkeypatch, n):
         out.append((fr.tile_start.clone(), fr.tile_end.clone(), fr.order.clone(), fr.out_img.clone()))
     for a, b in zip(out[0], out[1]):
         assert torch.equal(a, b)
+
+
+def test_culled_binning_edge_cases():
+    """Culled binning on degenerate views -- sub-pixel splats (only the footprint dilation
+    gives them extent) and a camera looking away from every splat (nothing kept): the frames
+    equal the reference lists', the culled lists are no longer (empty when nothing is kept),
+    and graph-replayed training steps on such views equal the eager ones."""
+    import dataclasses
+
+    from paper_2504_13339_b200 import scenes
+    from paper_2504_13339_b200.device import DeviceTF, Rasterizer
+    from paper_2504_13339_b200.train import TrainConfig, Trainer, View
+
+    gs = scenes.random_gaussians(3000, seed=21)
+    gs.log_scale[:] = -9.0  # far below a pixel: only the footprint dilation gives extent
+    tf = DeviceTF(scenes.random_tf(2, 4))
+    cam = scenes.orbit_cameras(1, 3, 96, 80)[0]
+    away = dataclasses.replace(cam, target=tuple(2 * p - t for p, t in zip(cam.position, cam.target)))
+    params = torch.from_numpy(gs.pack()).cuda()
+    for c in (cam, away):
+        ref = Rasterizer(pooled=False).forward(params, len(gs), tf, c)
+        cut = Rasterizer(pooled=False, cull=True).forward(params, len(gs), tf, c)
+        assert torch.equal(ref.out_img, cut.out_img) and torch.equal(ref.out_t, cut.out_t)
+        assert int(cut.tile_end.max()) <= int(ref.tile_end.max())
+        if c is away:
+            assert int(ref.tile_end.max()) == 0 and int(cut.tile_end.max()) == 0
+    target = torch.rand(cam.height, cam.width, 3, device="cuda")
+    views = [View(cam, tf, target), View(away, tf, target)]
+    res = []
+    for graphs in (False, True):
+        tr = Trainer(gs, TrainConfig(iterations=100), graphs=graphs)
+        losses = [float(tr.step(views, iteration=s + 1).item()) for s in range(3)]
+        res.append((losses, tr.params.clone()))
+    assert res[0][0] == res[1][0] and torch.equal(res[0][1], res[1][1])
