@@ -96,9 +96,12 @@ def init_from_env(backend: str = "nccl") -> tuple[int, int, int]:
     if world > 1 and not dist.is_initialized():
         if backend == "nccl":
             # NCCL's init lines (communicator, nranks, transport) stay in the job log unless
-            # the user chose a level
-            os.environ.setdefault("NCCL_DEBUG", "INFO")
-            os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+            # the user chose a level -- on stderr, so rank 0's JSON line stays the last line
+            # of stdout
+            if "NCCL_DEBUG" not in os.environ:
+                os.environ["NCCL_DEBUG"] = "INFO"
+                os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+                os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
             torch.cuda.set_device(local)
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         else:
