@@ -253,9 +253,11 @@ __global__ void __launch_bounds__(kSmallSortT) small_sort_kernel(const uint32_t 
     constexpr int NW = kSmallSortT / 32, IT = kSmallSortItems;
     __shared__ uint32_t s_wc[NW][256];
     __shared__ uint32_t s_dstart[256];
+    __shared__ int s_same;
     extern __shared__ uint32_t s_kv[];  // keys [0, n), ids [kSmallSort, kSmallSort + n)
     const int t = threadIdx.x, lane = t & 31, w = t >> 5;
     const int items = (n + kSmallSortT - 1) / kSmallSortT;  // per thread (<= IT)
+    if (t == 0) s_same = 0;
     uint32_t key[IT], val[IT];
 #pragma unroll
     for (int i = 0; i < IT; ++i) {
@@ -291,8 +293,14 @@ __global__ void __launch_bounds__(kSmallSortT) small_sort_kernel(const uint32_t 
                 cnt += c;
             }
             s_dstart[t] = cnt;
+            if (cnt == (uint32_t)n) s_same = 1;  // every key has this digit: the pass is the identity
         }
         __syncthreads();
+        if (s_same && pass < 3) {  // (stable: nothing moves) -- the next digit, same registers
+            __syncthreads();
+            if (t == 0) s_same = 0;
+            continue;
+        }
         if (t < 32) {  // exclusive sum of the 256 digit totals (8 per lane)
             uint32_t v[8], sum = 0;
 #pragma unroll
